@@ -1,0 +1,158 @@
+/* hawkes_b200.h — C ABI of the B200 spatiotemporal-Hawkes likelihood engine.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/hawkes/, "hphawkes"):
+ *
+ *   reference entry point                         replaced by
+ *   ----------------------------------------------------------------------
+ *   log_likelihood(Catalog, HawkesParams,          hk_create + hk_eval
+ *     Partition, Precision)     engine.hpp:101-110   (grad5 == NULL: LL only)
+ *   log_likelihood_t / slice_log_likelihood        hk_eval_rows
+ *                               engine.hpp:65-99
+ *   event_contribution          model.hpp:351-356  hk_eval_rows(b, b+1)
+ *   LikelihoodWorkspace<double>::set_locations     hk_set_locations
+ *                               engine.hpp:172-178
+ *   LikelihoodWorkspace<double>::evaluate_*        hk_eval (full O(N^2) pass)
+ *                               engine.hpp:133-158
+ *   Partition::make             engine.hpp:27-40   hk_partition_make
+ *   benchmark_catalog           engine.hpp:251-259 hk_benchmark_catalog
+ *   (new, no reference counterpart)                hk_eval with grad5 != NULL,
+ *                                                  hk_plan_shards
+ *
+ * Conventions (mirroring the reference's C++ error behaviour):
+ *   return 0 = ok, 1 = invalid_argument, 2 = out_of_range,
+ *          3 = CUDA runtime error, 4 = not implemented (e.g. single precision).
+ *   hk_last_error() returns the thread-local message of the last failure; the
+ *   messages for invalid inputs are the reference's own (types.hpp:45-55,
+ *   :92-103; engine.hpp:28-29).
+ *   Non-finite log-likelihood values are returned as values, not errors
+ *   (the reference's caller rejects them, mcmc.hpp:168).
+ *   A context is single-caller (like LikelihoodWorkspace); several contexts may
+ *   coexist.  Results are bitwise deterministic for a fixed (catalog, params,
+ *   device set).
+ *
+ * All arrays are host pointers unless the name says `device`.  No CUDA or
+ * torch types appear in the signatures; streams are passed as void*.
+ */
+#ifndef HAWKES_B200_H
+#define HAWKES_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HK_OK 0
+#define HK_INVALID_ARGUMENT 1
+#define HK_OUT_OF_RANGE 2
+#define HK_RUNTIME_ERROR 3
+#define HK_NOT_IMPLEMENTED 4
+
+#define HK_VARIANT_CONSTANT 0 /* Variant::constant, types.hpp:16 */
+#define HK_VARIANT_VARYING 1  /* Variant::varying */
+
+/* HawkesParams (types.hpp:83-110).  All six must be positive and finite. */
+typedef struct hk_params {
+  double mu0;     /* background weight */
+  double tau_t;   /* background temporal lengthscale (weeks) */
+  double xi0;     /* self-excitatory weight */
+  double sigma_x; /* triggering spatial lengthscale (degrees) */
+  double sigma_t; /* triggering temporal lengthscale (weeks) */
+  double area;    /* A, square degrees */
+  int variant;    /* HK_VARIANT_* */
+} hk_params;
+
+typedef struct hk_ctx hk_ctx;
+
+/* Builds an evaluation context for a time-sorted catalog (Catalog,
+ * types.hpp:41-78; the same validation and messages).  Copies the arrays,
+ * uploads them to `n_gpus` devices (0..n_gpus-1; 0 means 1) and plans
+ * cost-balanced row shards, one per device.  `density` is the per-event
+ * population density (Event::density); the variant is chosen per
+ * evaluation by hk_params.variant. */
+int hk_create(const double* t, const double* lon, const double* lat, const double* density,
+              size_t n, int n_gpus, hk_ctx** out);
+
+/* One rank's shard for a one-process-per-GPU job: the full catalog is
+ * uploaded to `device`, but only rows [row_begin, row_end) are evaluated.
+ * hk_eval then returns this shard's partial sums; the caller reduces the
+ * partials across ranks (in rank order, for determinism). */
+int hk_create_shard(const double* t, const double* lon, const double* lat, const double* density,
+                    size_t n, size_t row_begin, size_t row_end, int device, hk_ctx** out);
+
+void hk_destroy(hk_ctx* ctx);
+
+/* Replaces the event locations (LikelihoodWorkspace::set_locations,
+ * engine.hpp:172-178): host arrays of length n, copied to every device. */
+int hk_set_locations(hk_ctx* ctx, const double* lon, const double* lat);
+
+/* Same, from device arrays already resident on the context's device (e.g.
+ * after an NCCL broadcast); single-device contexts only. */
+int hk_set_locations_device(hk_ctx* ctx, const double* lon_device, const double* lat_device);
+
+/* Full evaluation.  *ll receives the log-likelihood (sum over the context's
+ * rows of ell_n, engine.hpp:65-99 / model.hpp:340-349).  If grad5 != NULL it
+ * receives d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t).  Synchronous. */
+int hk_eval(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5);
+
+/* Asynchronous form: enqueues the evaluation on the context's stream and
+ * leaves [ll, g_mu0, g_tau_t, g_xi0, g_sigma_x, g_sigma_t] in a device buffer
+ * (hk_result_device).  Single-device contexts only. */
+int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad);
+/* Device pointer to the 6-double result of the last hk_eval_async. */
+const double* hk_result_device(hk_ctx* ctx);
+/* cudaStream_t (as void*) the context launches on, for device index `dev`. */
+void* hk_stream(hk_ctx* ctx, int dev);
+
+/* Per-row contributions ell_n for rows [b, e) (slice_log_likelihood on
+ * single rows, engine.hpp:65-83).  ell_rows has e-b entries; grad_rows, if
+ * non-NULL, has 5*(e-b) entries (row-major, 5 per row).  Rows must lie in
+ * the context's row range, else HK_OUT_OF_RANGE. */
+int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* ell_rows,
+                 double* grad_rows);
+
+/* Rows [begin, end) this context evaluates, and its device count. */
+int hk_rows(const hk_ctx* ctx, size_t* begin, size_t* end, int* n_devices);
+
+/* Device-side timing of the pair kernel (CUDA events on the launching
+ * stream).  Enable before evaluating; read back accumulated milliseconds,
+ * the number of pair-kernel launches, and the number of all kernel
+ * launches this library made since the last reset. */
+int hk_set_profiling(hk_ctx* ctx, int enable);
+int hk_profile(hk_ctx* ctx, double* pair_kernel_ms, long* pair_launches, long* total_launches);
+int hk_reset_profile(hk_ctx* ctx);
+
+/* Catalog invariants (types.hpp:43-57) and HawkesParams::validate
+ * (types.hpp:92-103) on their own, with the reference's messages. */
+int hk_validate_catalog(const double* t, const double* lon, const double* lat,
+                        const double* density, size_t n);
+int hk_validate_params(const hk_params* p);
+
+/* Partition::make (engine.hpp:27-40) as g+1 boundaries. */
+int hk_partition_make(size_t n, size_t g, size_t* bounds);
+
+/* Cost-balanced contiguous row shards for g devices: boundaries (g+1) such
+ * that each shard carries ~1/g of the pair work, row n costing
+ * alpha*(N-1) + beta*count_before(t_n). */
+int hk_plan_shards(const double* t, size_t n, size_t g, size_t* bounds);
+
+/* benchmark_catalog(n, seed) (engine.hpp:251-259): the reference's
+ * synthetic uniform catalog, bit-identical (mt19937_64, libstdc++
+ * uniform_real_distribution, stable sort by t). */
+int hk_benchmark_catalog(size_t n, uint64_t seed, double* t, double* lon, double* lat,
+                         double* density);
+
+/* Measured FP64 FMA throughput of `device` in TFLOP/s (2 flop per DFMA),
+ * from a short register-resident DFMA loop; the roofline denominator. */
+int hk_measure_fp64_peak(int device, double* tflops, double* ms);
+
+const char* hk_last_error(void);
+const char* hk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HAWKES_B200_H */

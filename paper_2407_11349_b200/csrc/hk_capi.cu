@@ -1,0 +1,526 @@
+// C ABI (include/hawkes_b200.h): evaluation contexts over one or more B200s.
+//
+// A context holds, per device, a full replica of the catalog in SoA form
+// (t, lon, lat, density; padded to whole 256-column tiles), the tie bounds
+// lb/ub, the per-evaluation prep arrays, the work-item list for that
+// device's row shard, and the partial-sum buffer.  Catalog data are
+// uploaded once (hk_create) and locations replaced in place
+// (hk_set_locations), matching LikelihoodWorkspace's lifetime
+// (engine.hpp:117-229).  Multi-device contexts evaluate their shards
+// concurrently (one stream per device) and sum the per-device 6-vectors on
+// the host in device order, so the result is deterministic.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hawkes_b200.h"
+#include "hk_device.cuh"
+#include "hk_host.hpp"
+#include "hk_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NotImplemented : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return HK_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return HK_INVALID_ARGUMENT;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return HK_OUT_OF_RANGE;
+  } catch (const NotImplemented& e) {
+    g_err = e.what();
+    return HK_NOT_IMPLEMENTED;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HK_RUNTIME_ERROR;
+  }
+}
+
+template <typename T>
+T* dmalloc(std::size_t count) {
+  void* p = nullptr;
+  ck(cudaMalloc(&p, std::max<std::size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+struct DeviceState {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  int rb = 0, re = 0;  // row shard
+  double *t = nullptr, *x = nullptr, *y = nullptr, *q = nullptr;
+  double *K = nullptr, *thr = nullptr, *w = nullptr, *v = nullptr, *z = nullptr;
+  int *lb = nullptr, *ub = nullptr;
+  hk::Item* items = nullptr;
+  int n_items = 0, slots = 0;
+  double* partial = nullptr;
+  double* blockpart = nullptr;
+  int n_finish_blocks = 0;
+  double* out6 = nullptr;
+  double* h_out6 = nullptr;  // pinned
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  std::size_t prof_used = 0;
+
+  hk::DeviceCatalog catalog(int n, int npad) const {
+    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z};
+  }
+};
+
+}  // namespace
+
+struct hk_ctx {
+  int n = 0, npad = 0;
+  std::vector<double> t, x, y, d;
+  std::vector<int> lb, ub;
+  double d2_max = 0.0, q_max = 1.0;
+  std::vector<DeviceState> devs;
+  bool profiling = false;
+  double prof_ms = 0.0;
+  long prof_pair = 0, prof_total = 0;
+
+  ~hk_ctx() {
+    for (auto& s : devs) {
+      cudaSetDevice(s.dev);
+      if (s.stream) cudaStreamSynchronize(s.stream);
+      for (double* p : {s.t, s.x, s.y, s.q, s.K, s.thr, s.w, s.v, s.z, s.partial, s.blockpart, s.out6})
+        if (p) cudaFree(p);
+      if (s.lb) cudaFree(s.lb);
+      if (s.ub) cudaFree(s.ub);
+      if (s.items) cudaFree(s.items);
+      if (s.h_out6) cudaFreeHost(s.h_out6);
+      for (auto& e : s.prof_events) {
+        cudaEventDestroy(e.first);
+        cudaEventDestroy(e.second);
+      }
+      if (s.stream) cudaStreamDestroy(s.stream);
+    }
+  }
+
+  void update_bbox() {
+    double xmin = x[0], xmax = x[0], ymin = y[0], ymax = y[0];
+    for (int i = 1; i < n; ++i) {
+      xmin = std::min(xmin, x[i]);
+      xmax = std::max(xmax, x[i]);
+      ymin = std::min(ymin, y[i]);
+      ymax = std::max(ymax, y[i]);
+    }
+    const double w = xmax - xmin, h = ymax - ymin;
+    d2_max = w * w + h * h;
+  }
+
+  void upload_padded(DeviceState& s, double* dst, const std::vector<double>& src, double pad) {
+    std::vector<double> tmp(npad, pad);
+    std::copy(src.begin(), src.end(), tmp.begin());
+    ck(cudaMemcpyAsync(dst, tmp.data(), npad * sizeof(double), cudaMemcpyHostToDevice, s.stream),
+       "upload");
+    ck(cudaStreamSynchronize(s.stream), "upload sync");
+  }
+
+  void init_device(DeviceState& s, int dev, int rb, int re) {
+    s.dev = dev;
+    s.rb = rb;
+    s.re = re;
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    s.t = dmalloc<double>(npad);
+    s.x = dmalloc<double>(npad);
+    s.y = dmalloc<double>(npad);
+    s.q = dmalloc<double>(npad);
+    s.K = dmalloc<double>(npad);
+    s.thr = dmalloc<double>(npad);
+    s.w = dmalloc<double>(npad);
+    s.v = dmalloc<double>(npad);
+    s.z = dmalloc<double>(npad);
+    s.lb = dmalloc<int>(n);
+    s.ub = dmalloc<int>(n);
+    upload_padded(s, s.t, t, t[n - 1]);
+    upload_padded(s, s.x, x, 0.0);
+    upload_padded(s, s.y, y, 0.0);
+    upload_padded(s, s.q, d, 1.0);
+    ck(cudaMemcpy(s.lb, lb.data(), n * sizeof(int), cudaMemcpyHostToDevice), "upload lb");
+    ck(cudaMemcpy(s.ub, ub.data(), n * sizeof(int), cudaMemcpyHostToDevice), "upload ub");
+    std::vector<hk::Item> items;
+    s.slots = hk::plan_items(lb, ub, n, rb, re, items);
+    s.n_items = static_cast<int>(items.size());
+    s.items = dmalloc<hk::Item>(items.size());
+    ck(cudaMemcpy(s.items, items.data(), items.size() * sizeof(hk::Item), cudaMemcpyHostToDevice),
+       "upload items");
+    const std::size_t rows = static_cast<std::size_t>(re - rb);
+    s.partial = dmalloc<double>(static_cast<std::size_t>(s.slots) * 5 * rows);
+    s.n_finish_blocks = static_cast<int>((rows + 255) / 256);
+    s.blockpart = dmalloc<double>(static_cast<std::size_t>(s.n_finish_blocks) * 6);
+    s.out6 = dmalloc<double>(6);
+    ck(cudaMallocHost(&s.h_out6, 6 * sizeof(double)), "cudaMallocHost");
+  }
+
+  std::pair<cudaEvent_t, cudaEvent_t> next_events(DeviceState& s) {
+    if (s.prof_used == s.prof_events.size()) {
+      cudaEvent_t a, b;
+      ck(cudaEventCreate(&a), "cudaEventCreate");
+      ck(cudaEventCreate(&b), "cudaEventCreate");
+      s.prof_events.emplace_back(a, b);
+    }
+    return s.prof_events[s.prof_used++];
+  }
+
+  hk::EvalCoef coef(const hk_params* p) const {
+    if (!p) throw std::invalid_argument("hk_eval: null params");
+    const hk::ParamsIn in{p->mu0, p->tau_t, p->xi0, p->sigma_x, p->sigma_t, p->area, p->variant};
+    hk::validate_params(in);
+    return hk::make_coef(in, t[0], t[n - 1], d2_max, q_max);
+  }
+
+  // Enqueues prep + pair + finish + reduce for device s.
+  void enqueue(DeviceState& s, const hk::EvalCoef& c, bool grad) {
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    const hk::DeviceCatalog dc = s.catalog(n, npad);
+    hk::launch_prep(dc, c, s.stream);
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    if (profiling) {
+      ev = next_events(s);
+      ck(cudaEventRecord(ev.first, s.stream), "cudaEventRecord");
+    }
+    hk::launch_pair(dc, c, s.items, s.n_items, s.partial, s.rb, s.re - s.rb, grad, s.stream);
+    if (profiling) ck(cudaEventRecord(ev.second, s.stream), "cudaEventRecord");
+    hk::launch_finish(dc, c, s.partial, s.slots, s.rb, s.re - s.rb, grad, nullptr, nullptr,
+                      s.blockpart, s.stream);
+    hk::launch_reduce(s.blockpart, s.n_finish_blocks, s.out6, s.stream);
+    ck(cudaGetLastError(), "kernel launch");
+    if (profiling) prof_pair += 1;
+    prof_total += 4;
+  }
+};
+
+namespace {
+
+std::unique_ptr<hk_ctx> new_ctx(const double* t, const double* x, const double* y,
+                                const double* d, std::size_t n) {
+  if (!t || !x || !y || !d) throw std::invalid_argument("hk_create: null array");
+  hk::validate_catalog(t, x, y, d, n);
+  auto ctx = std::make_unique<hk_ctx>();
+  ctx->n = static_cast<int>(n);
+  ctx->npad = static_cast<int>((n + hk::kBJ - 1) / hk::kBJ * hk::kBJ);
+  ctx->t.assign(t, t + n);
+  ctx->x.assign(x, x + n);
+  ctx->y.assign(y, y + n);
+  ctx->d.assign(d, d + n);
+  ctx->q_max = *std::max_element(ctx->d.begin(), ctx->d.end());
+  hk::tie_bounds(ctx->t, ctx->lb, ctx->ub);
+  ctx->update_bbox();
+  return ctx;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hk_last_error(void) { return g_err.c_str(); }
+const char* hk_version(void) { return "hawkes_b200 0.1 (sm_100a)"; }
+
+int hk_create(const double* t, const double* lon, const double* lat, const double* density,
+              size_t n, int n_gpus, hk_ctx** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("hk_create: null output");
+    *out = nullptr;
+    auto ctx = new_ctx(t, lon, lat, density, n);
+    int avail = 0;
+    ck(cudaGetDeviceCount(&avail), "cudaGetDeviceCount");
+    const int g = n_gpus <= 0 ? 1 : n_gpus;
+    if (g > avail)
+      throw std::invalid_argument("hk_create: requested " + std::to_string(g) +
+                                  " GPUs, " + std::to_string(avail) + " visible");
+    if (static_cast<std::size_t>(g) > n) throw std::invalid_argument("Partition: more workers than terms");
+    const auto bounds = hk::plan_shards(ctx->lb, static_cast<std::size_t>(g));
+    ctx->devs.resize(g);
+    for (int i = 0; i < g; ++i)
+      ctx->init_device(ctx->devs[i], i, static_cast<int>(bounds[i]), static_cast<int>(bounds[i + 1]));
+    *out = ctx.release();
+  });
+}
+
+int hk_create_shard(const double* t, const double* lon, const double* lat, const double* density,
+                    size_t n, size_t row_begin, size_t row_end, int device, hk_ctx** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("hk_create_shard: null output");
+    *out = nullptr;
+    auto ctx = new_ctx(t, lon, lat, density, n);
+    if (!(row_begin < row_end) || row_end > n)
+      throw std::out_of_range("hk_create_shard: row range out of range");
+    int avail = 0;
+    ck(cudaGetDeviceCount(&avail), "cudaGetDeviceCount");
+    if (device < 0 || device >= avail) throw std::invalid_argument("hk_create_shard: bad device");
+    ctx->devs.resize(1);
+    ctx->init_device(ctx->devs[0], device, static_cast<int>(row_begin), static_cast<int>(row_end));
+    *out = ctx.release();
+  });
+}
+
+void hk_destroy(hk_ctx* ctx) { delete ctx; }
+
+int hk_set_locations(hk_ctx* ctx, const double* lon, const double* lat) {
+  return guarded([&] {
+    if (!ctx || !lon || !lat) throw std::invalid_argument("hk_set_locations: null argument");
+    for (int i = 0; i < ctx->n; ++i)
+      if (!std::isfinite(lon[i]) || !std::isfinite(lat[i]))
+        throw std::invalid_argument("Catalog: event " + std::to_string(i) +
+                                    " has non-finite location");
+    std::copy(lon, lon + ctx->n, ctx->x.begin());
+    std::copy(lat, lat + ctx->n, ctx->y.begin());
+    ctx->update_bbox();
+    for (auto& s : ctx->devs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaMemcpyAsync(s.x, lon, ctx->n * sizeof(double), cudaMemcpyHostToDevice, s.stream),
+         "set_locations");
+      ck(cudaMemcpyAsync(s.y, lat, ctx->n * sizeof(double), cudaMemcpyHostToDevice, s.stream),
+         "set_locations");
+    }
+  });
+}
+
+int hk_set_locations_device(hk_ctx* ctx, const double* lon_device, const double* lat_device) {
+  return guarded([&] {
+    if (!ctx || !lon_device || !lat_device)
+      throw std::invalid_argument("hk_set_locations_device: null argument");
+    if (ctx->devs.size() != 1)
+      throw std::invalid_argument("hk_set_locations_device: single-device contexts only");
+    auto& s = ctx->devs[0];
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    ck(cudaMemcpyAsync(s.x, lon_device, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, s.stream),
+       "set_locations_device");
+    ck(cudaMemcpyAsync(s.y, lat_device, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, s.stream),
+       "set_locations_device");
+    // Host mirror for the argument bound (bbox) and hk_eval_rows.
+    ck(cudaMemcpyAsync(ctx->x.data(), lon_device, ctx->n * sizeof(double), cudaMemcpyDeviceToHost,
+                       s.stream),
+       "mirror");
+    ck(cudaMemcpyAsync(ctx->y.data(), lat_device, ctx->n * sizeof(double), cudaMemcpyDeviceToHost,
+                       s.stream),
+       "mirror");
+    ck(cudaStreamSynchronize(s.stream), "mirror sync");
+    ctx->update_bbox();
+  });
+}
+
+int hk_eval(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5) {
+  return guarded([&] {
+    if (!ctx || !ll) throw std::invalid_argument("hk_eval: null argument");
+    const hk::EvalCoef c = ctx->coef(p);
+    const bool grad = grad5 != nullptr;
+    for (auto& s : ctx->devs) {
+      ctx->enqueue(s, c, grad);
+      ck(cudaMemcpyAsync(s.h_out6, s.out6, 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
+         "result copy");
+    }
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (auto& s : ctx->devs) {  // device order: deterministic
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaStreamSynchronize(s.stream), "hk_eval");
+      for (int k = 0; k < 6; ++k) acc[k] += s.h_out6[k];
+    }
+    *ll = acc[0];
+    if (grad5)
+      for (int k = 0; k < 5; ++k) grad5[k] = acc[1 + k];
+  });
+}
+
+int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("hk_eval_async: null context");
+    if (ctx->devs.size() != 1)
+      throw std::invalid_argument("hk_eval_async: single-device contexts only");
+    const hk::EvalCoef c = ctx->coef(p);
+    ctx->enqueue(ctx->devs[0], c, with_grad != 0);
+  });
+}
+
+const double* hk_result_device(hk_ctx* ctx) {
+  return (ctx && !ctx->devs.empty()) ? ctx->devs[0].out6 : nullptr;
+}
+
+void* hk_stream(hk_ctx* ctx, int dev) {
+  if (!ctx || dev < 0 || dev >= static_cast<int>(ctx->devs.size())) return nullptr;
+  return static_cast<void*>(ctx->devs[dev].stream);
+}
+
+int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* ell_rows,
+                 double* grad_rows) {
+  return guarded([&] {
+    if (!ctx || !ell_rows) throw std::invalid_argument("hk_eval_rows: null argument");
+    const hk::EvalCoef c = ctx->coef(p);
+    if (!(b < e) || e > static_cast<size_t>(ctx->n))
+      throw std::out_of_range("event_contribution: index out of range");
+    // the device whose shard contains the range
+    DeviceState* sp = nullptr;
+    for (auto& s : ctx->devs)
+      if (b >= static_cast<size_t>(s.rb) && e <= static_cast<size_t>(s.re)) sp = &s;
+    if (!sp) throw std::out_of_range("hk_eval_rows: rows outside this context's shard");
+    DeviceState& s = *sp;
+    ck(cudaSetDevice(s.dev), "cudaSetDevice");
+    const int rb = static_cast<int>(b), re = static_cast<int>(e);
+    std::vector<hk::Item> items;
+    const int slots = hk::plan_items(ctx->lb, ctx->ub, ctx->n, rb, re, items);
+    const std::size_t rows = e - b;
+    hk::Item* d_items = dmalloc<hk::Item>(items.size());
+    double* d_partial = dmalloc<double>(static_cast<std::size_t>(slots) * 5 * rows);
+    double* d_ell = dmalloc<double>(rows);
+    double* d_grad = dmalloc<double>(rows * 5);
+    const int nfb = static_cast<int>((rows + 255) / 256);
+    double* d_bp = dmalloc<double>(static_cast<std::size_t>(nfb) * 6);
+    auto cleanup = [&] {
+      cudaFree(d_items);
+      cudaFree(d_partial);
+      cudaFree(d_ell);
+      cudaFree(d_grad);
+      cudaFree(d_bp);
+    };
+    try {
+      ck(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(hk::Item),
+                         cudaMemcpyHostToDevice, s.stream),
+         "items");
+      const hk::DeviceCatalog dc = s.catalog(ctx->n, ctx->npad);
+      hk::launch_prep(dc, c, s.stream);
+      const bool grad = grad_rows != nullptr;
+      hk::launch_pair(dc, c, d_items, static_cast<int>(items.size()), d_partial, rb, re - rb, grad,
+                      s.stream);
+      hk::launch_finish(dc, c, d_partial, slots, rb, re - rb, grad, d_ell, grad ? d_grad : nullptr,
+                        d_bp, s.stream);
+      ck(cudaGetLastError(), "kernel launch");
+      ctx->prof_total += 3;
+      ck(cudaMemcpyAsync(ell_rows, d_ell, rows * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
+         "rows copy");
+      if (grad)
+        ck(cudaMemcpyAsync(grad_rows, d_grad, rows * 5 * sizeof(double), cudaMemcpyDeviceToHost,
+                           s.stream),
+           "rows copy");
+      ck(cudaStreamSynchronize(s.stream), "hk_eval_rows");
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+int hk_rows(const hk_ctx* ctx, size_t* begin, size_t* end, int* n_devices) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("hk_rows: null context");
+    if (begin) *begin = static_cast<size_t>(ctx->devs.front().rb);
+    if (end) *end = static_cast<size_t>(ctx->devs.back().re);
+    if (n_devices) *n_devices = static_cast<int>(ctx->devs.size());
+  });
+}
+
+int hk_set_profiling(hk_ctx* ctx, int enable) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("hk_set_profiling: null context");
+    ctx->profiling = enable != 0;
+  });
+}
+
+int hk_profile(hk_ctx* ctx, double* pair_kernel_ms, long* pair_launches, long* total_launches) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("hk_profile: null context");
+    double ms = 0.0;
+    for (auto& s : ctx->devs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaStreamSynchronize(s.stream), "hk_profile");
+      for (std::size_t i = 0; i < s.prof_used; ++i) {
+        float m = 0.f;
+        ck(cudaEventElapsedTime(&m, s.prof_events[i].first, s.prof_events[i].second),
+           "cudaEventElapsedTime");
+        ms += m;
+      }
+    }
+    if (pair_kernel_ms) *pair_kernel_ms = ms;
+    if (pair_launches) *pair_launches = ctx->prof_pair;
+    if (total_launches) *total_launches = ctx->prof_total;
+  });
+}
+
+int hk_reset_profile(hk_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("hk_reset_profile: null context");
+    for (auto& s : ctx->devs) s.prof_used = 0;
+    ctx->prof_pair = 0;
+    ctx->prof_total = 0;
+  });
+}
+
+int hk_validate_catalog(const double* t, const double* lon, const double* lat,
+                        const double* density, size_t n) {
+  return guarded([&] {
+    if (!t || !lon || !lat || !density) throw std::invalid_argument("hk_validate_catalog: null array");
+    hk::validate_catalog(t, lon, lat, density, n);
+  });
+}
+
+int hk_validate_params(const hk_params* p) {
+  return guarded([&] {
+    if (!p) throw std::invalid_argument("hk_validate_params: null params");
+    hk::validate_params(
+        hk::ParamsIn{p->mu0, p->tau_t, p->xi0, p->sigma_x, p->sigma_t, p->area, p->variant});
+  });
+}
+
+int hk_partition_make(size_t n, size_t g, size_t* bounds) {
+  return guarded([&] {
+    if (!bounds) throw std::invalid_argument("hk_partition_make: null output");
+    const auto b = hk::partition_make(n, g);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
+int hk_plan_shards(const double* t, size_t n, size_t g, size_t* bounds) {
+  return guarded([&] {
+    if (!t || !bounds) throw std::invalid_argument("hk_plan_shards: null argument");
+    std::vector<double> tv(t, t + n);
+    for (size_t i = 1; i < n; ++i)
+      if (tv[i - 1] > tv[i])
+        throw std::invalid_argument("Catalog: times not sorted at index " + std::to_string(i));
+    std::vector<int> lb, ub;
+    hk::tie_bounds(tv, lb, ub);
+    const auto b = hk::plan_shards(lb, g);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
+int hk_benchmark_catalog(size_t n, uint64_t seed, double* t, double* lon, double* lat,
+                         double* density) {
+  return guarded([&] {
+    if (!t || !lon || !lat || !density) throw std::invalid_argument("hk_benchmark_catalog: null array");
+    hk::benchmark_catalog(n, seed, t, lon, lat, density);
+  });
+}
+
+int hk_measure_fp64_peak(int device, double* tflops, double* ms) {
+  return guarded([&] {
+    if (!tflops) throw std::invalid_argument("hk_measure_fp64_peak: null output");
+    *tflops = hk::measure_fp64_peak(device, ms);
+    ck(cudaGetLastError(), "dfma probe");
+  });
+}
+
+}  // extern "C"

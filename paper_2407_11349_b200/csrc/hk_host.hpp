@@ -1,0 +1,52 @@
+// Host-side logic behind the C ABI: validation with the reference's
+// messages, the reference's synthetic catalog, partitions and shard plans,
+// and the work-item planner for the pair kernel.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hk_kernels.cuh"
+
+namespace hk {
+
+struct ParamsIn {
+  double mu0, tau_t, xi0, sigma_x, sigma_t, area;
+  int variant;
+};
+
+// Catalog invariants, types.hpp:43-57 (same checks, same messages).
+void validate_catalog(const double* t, const double* x, const double* y, const double* d,
+                      std::size_t n);
+// HawkesParams::validate, types.hpp:92-103.
+void validate_params(const ParamsIn& p);
+
+// benchmark_catalog(n, seed), engine.hpp:251-259.
+void benchmark_catalog(std::size_t n, std::uint64_t seed, double* t, double* x, double* y,
+                       double* d);
+
+// Partition::make, engine.hpp:27-40, as g+1 boundaries.
+std::vector<std::size_t> partition_make(std::size_t n, std::size_t g);
+
+// count_before / upper_bound for every row of a sorted time array.
+void tie_bounds(const std::vector<double>& t, std::vector<int>& lb, std::vector<int>& ub);
+
+// Cost-balanced contiguous shards: row i costs kAlpha*(n-1) + kBeta*lb[i].
+constexpr double kCostAlpha = 13.0;  // FP64 instructions per background pair
+constexpr double kCostBeta = 17.0;   // FP64 instructions per trigger pair
+std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g);
+
+// Work items for rows [rb, re) of an n-event catalog: row blocks of kBI
+// rows times column chunks of whole tiles; heaviest first.  Returns the
+// number of chunk slots per row.
+int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
+               std::vector<Item>& items);
+
+// Per-evaluation coefficients (types.hpp:105-109, model.hpp:328-336) and
+// the host-side argument bound that selects the checked exp.
+EvalCoef make_coef(const ParamsIn& p, double t_min, double t_max, double d2_max, double q_max);
+
+}  // namespace hk

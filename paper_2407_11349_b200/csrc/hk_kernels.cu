@@ -1,0 +1,574 @@
+// sm_100a kernels for the StHP log-likelihood and its gradient.
+//
+// Per evaluation (one stream, four launches):
+//   1. prep   O(N)    per-source trigger coefficients, tile-relative temporal
+//                     weights w_j, and the skip thresholds.
+//   2. pair   O(N^2)  one CTA per work item (256 rows x a range of 256-column
+//                     tiles).  Rows live in registers (2 per thread); column
+//                     tiles are staged in shared memory with bulk-async
+//                     copies (cp.async.bulk + mbarrier, double-buffered).
+//                     Five FP64 accumulators per row:
+//                       B  = sum_{t_j != t_i} b_ij          (model.hpp:250-266)
+//                       B2 = sum (t_i-t_j)^2 b_ij            (gradient, new)
+//                       T  = sum_{t_j < t_i} g_ij            (model.hpp:272-296)
+//                       Td = sum (t_i-t_j) g_ij              (gradient, new)
+//                       Tq = sum q_j d_ij^2 g_ij             (gradient, new)
+//                     with b_ij = exp(-(t_i-t_j)^2 / 2 tau^2) and
+//                     g_ij = q_j exp(-omega (t_i-t_j) - q_j d_ij^2 / 2 sigma_x^2).
+//   3. finish O(N)    combines partial slots in a fixed order, forms
+//                     ell_n = log(max(S_n, 1e-40)) - Lambda_n (model.hpp:301-349)
+//                     and d ell_n / d theta, block-reduces to 6 doubles.
+//   4. reduce         fixed-order sum of the block partials.
+// No floating-point atomics anywhere: results are bitwise deterministic.
+//
+// Column tiles fall in four classes, decided per CTA from the sorted times
+// (uniform across the CTA, so no divergence):
+//   BT  every column strictly earlier than every row (j < count_before of
+//       the first row): background + trigger, no guards.  The trigger's
+//       temporal factor is split as exp(-omega(t_i - t_ref)) * w_j with
+//       t_ref the tile's last time, so the per-pair exponent is the spatial
+//       Gaussian alone and the row factor is applied once per tile.
+//   B   every column after every row's ties: background only, no guards.
+//   M   the band around the rows' own times: per-pair guards
+//       t_j != t_i (as j outside [lb_i, ub_i)) and t_j < t_i (j < lb_i),
+//       exactly the reference's value guards (model.hpp:263, :278).
+//   skip tiles whose every term flushes to zero in this arithmetic.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hk_device.cuh"
+#include "hk_kernels.cuh"
+
+namespace hk {
+
+namespace {
+
+enum TileType { kSkip = 0, kTileBT = 1, kTileB = 2, kTileT = 3, kTileM = 4 };
+
+// Shared-memory slots of one staged tile.
+enum Slot { sT = 0, sX, sY, sW, sV, sZ, sK, sAux, kSlots };
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "HK_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra HK_WAIT;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// 1-D bulk async copy global -> shared (TMA engine; SASS UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct PairParams {
+  DeviceCatalog d;
+  EvalCoef c;
+  const Item* items;
+  double* partial;
+  int rows_base, rows_total;
+};
+
+struct BlockInfo {
+  int rb, re, lbmin, ubmax;
+  double t_first, t_last;
+};
+
+__device__ __forceinline__ int tile_type(int J, const BlockInfo& bi, const PairParams& P) {
+  const int j0 = J * kBJ, j1 = j0 + kBJ;
+  const double* __restrict__ t = P.d.t;
+  if (j1 <= bi.lbmin) {
+    // columns strictly earlier than every row of the block
+    const double td = bi.t_first - t[j1 - 1];
+    const bool bg_far = td * td * (-P.c.Kb) > kFlushArg;
+    const bool tr_far = td * (-P.c.Kw) > kFlushArg;
+    return bg_far ? (tr_far ? kSkip : kTileT) : (tr_far ? kTileB : kTileBT);
+  }
+  if (j0 >= bi.ubmax && j1 <= P.d.n) {
+    const double td = t[j0] - bi.t_last;
+    return td * td * (-P.c.Kb) > kFlushArg ? kSkip : kTileB;
+  }
+  return kTileM;
+}
+
+template <bool kVarying, bool kGrad>
+__device__ __forceinline__ void issue_tile(int type, int J, double* buf, uint64_t* bar,
+                                           const PairParams& P) {
+  const int j0 = J * kBJ;
+  constexpr unsigned kBytes = kBJ * sizeof(double);
+  unsigned mask = 0;
+  if (type == kTileB) {
+    mask = 1u << sT;
+  } else if (type == kTileM) {
+    mask = (1u << sT) | (1u << sX) | (1u << sY);
+    if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = q
+  } else {  // BT or T
+    mask = (1u << sT) | (1u << sX) | (1u << sY) | (1u << sW);
+    if (kGrad) mask |= (1u << sV) | (1u << sZ);
+    if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = thr
+    if (kVarying && kGrad) mask |= (1u << sZ);
+  }
+  mbar_expect_tx(bar, kBytes * __popc(mask));
+  const double* src[kSlots] = {P.d.t, P.d.x, P.d.y, P.d.w, P.d.v, P.d.z, P.d.K,
+                               type == kTileM ? P.d.q : P.d.thr};
+#pragma unroll
+  for (int s = 0; s < kSlots; ++s)
+    if (mask & (1u << s)) bulk_g2s(buf + s * kBJ, src[s] + j0, kBytes, bar);
+}
+
+struct RowState {
+  double t[kRowsPerThread], x[kRowsPerThread], y[kRowsPerThread];
+  int lb[kRowsPerThread], ub[kRowsPerThread];
+  double B[kRowsPerThread], B2[kRowsPerThread], T[kRowsPerThread], Td[kRowsPerThread],
+      Tq[kRowsPerThread];
+};
+
+// BT / B / T tiles: no per-pair guards.
+template <bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr>
+__device__ __forceinline__ void tile_fast(RowState& R, const double* __restrict__ buf,
+                                          const EvalCoef& c) {
+  const double* __restrict__ st = buf + sT * kBJ;
+  const double* __restrict__ sx = buf + sX * kBJ;
+  const double* __restrict__ sy = buf + sY * kBJ;
+  const double* __restrict__ sw = buf + sW * kBJ;
+  const double* __restrict__ sv = buf + sV * kBJ;
+  const double* __restrict__ sz = buf + sZ * kBJ;
+  const double* __restrict__ sk = buf + sK * kBJ;
+  const double* __restrict__ sthr = buf + sAux * kBJ;
+  const double Kb = c.Kb, Kq0 = c.Kq0;
+  double Tp[kRowsPerThread], Vp[kRowsPerThread], Qp[kRowsPerThread];
+#pragma unroll
+  for (int r = 0; r < kRowsPerThread; ++r) Tp[r] = Vp[r] = Qp[r] = 0.0;
+
+#pragma unroll kUnroll
+  for (int j = 0; j < kBJ; ++j) {
+    if (kBg) {
+      const double tj = st[j];
+#pragma unroll
+      for (int r = 0; r < kRowsPerThread; ++r) {
+        const double td = R.t[r] - tj;
+        const double td2 = td * td;
+        const double b = exp2_16<kMode>(td2, Kb);
+        R.B[r] += b;
+        if (kGrad) R.B2[r] = fma(td2, b, R.B2[r]);
+      }
+    }
+    if (kTr) {
+      const double xj = sx[j], yj = sy[j], wj = sw[j];
+      const double Kj = kVarying ? sk[j] : Kq0;
+      double d2[kRowsPerThread];
+#pragma unroll
+      for (int r = 0; r < kRowsPerThread; ++r) {
+        const double dx = R.x[r] - xj, dy = R.y[r] - yj;
+        d2[r] = fma(dx, dx, dy * dy);
+      }
+      bool go = true;
+      if (kVarying) {
+        // Warp-uniform skip when every lane's spatial factor flushes to 0
+        // (d^2 above the per-source threshold; high-word integer compare
+        // of non-negative doubles is order-preserving and conservative).
+        const int thr_hi = __double2hiint(sthr[j]);
+        bool live = false;
+#pragma unroll
+        for (int r = 0; r < kRowsPerThread; ++r) live |= __double2hiint(d2[r]) <= thr_hi;
+        go = __any_sync(0xffffffffu, live);
+      }
+      if (go) {
+        const double vj = kGrad ? sv[j] : 0.0;
+        const double zj = kGrad ? (kVarying ? sz[j] : wj) : 0.0;
+#pragma unroll
+        for (int r = 0; r < kRowsPerThread; ++r) {
+          const double e = exp2_16<kMode>(d2[r], Kj);
+          Tp[r] = fma(wj, e, Tp[r]);
+          if (kGrad) {
+            Vp[r] = fma(vj, e, Vp[r]);
+            Qp[r] = fma(zj, d2[r] * e, Qp[r]);
+          }
+        }
+      }
+    }
+  }
+  if (kTr) {
+    const double t_ref = st[kBJ - 1];
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) {
+      const double dt = R.t[r] - t_ref;  // >= 0 on BT/T tiles
+      const double E = exp2_16<kMode>(dt, c.Kw);
+      R.T[r] = fma(E, Tp[r], R.T[r]);
+      if (kGrad) {
+        R.Td[r] = fma(E, fma(dt, Tp[r], Vp[r]), R.Td[r]);
+        R.Tq[r] = fma(E, Qp[r], R.Tq[r]);
+      }
+    }
+  }
+}
+
+// M tiles: the reference's exact value guards, per pair.
+template <bool kVarying, bool kGrad, int kMode>
+__device__ __forceinline__ void tile_masked(RowState& R, int j0, int n,
+                                            const double* __restrict__ buf, const EvalCoef& c) {
+  const double* __restrict__ st = buf + sT * kBJ;
+  const double* __restrict__ sx = buf + sX * kBJ;
+  const double* __restrict__ sy = buf + sY * kBJ;
+  const double* __restrict__ sk = buf + sK * kBJ;
+  const double* __restrict__ sq = buf + sAux * kBJ;
+  const double Kb = c.Kb, Kq0 = c.Kq0, Kw = c.Kw;
+#pragma unroll 1
+  for (int j = 0; j < kBJ; ++j) {
+    const int jg = j0 + j;
+    const double tj = st[j], xj = sx[j], yj = sy[j];
+    const double qj = kVarying ? sq[j] : 1.0;
+    const double Kj = kVarying ? sk[j] : Kq0;
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) {
+      const double td = R.t[r] - tj;
+      const double td2 = td * td;
+      double b = exp2_16<kMode>(td2, Kb);
+      const bool bg_ok = (jg < R.lb[r] || jg >= R.ub[r]) && jg < n;  // t_j != t_i
+      b = bg_ok ? b : 0.0;
+      R.B[r] += b;
+      if (kGrad) R.B2[r] = fma(td2, b, R.B2[r]);
+      const bool tr_ok = jg < R.lb[r];  // t_j < t_i
+      const double dx = R.x[r] - xj, dy = R.y[r] - yj;
+      const double d2 = fma(dx, dx, dy * dy);
+      const double A = fma(d2, Kj, td * Kw);
+      const double e = exp2_16_arg<kMode>(A);
+      const double g = tr_ok ? (kVarying ? e * qj : e) : 0.0;
+      R.T[r] += g;
+      if (kGrad) {
+        R.Td[r] = fma(td, g, R.Td[r]);
+        R.Tq[r] = fma(kVarying ? qj * d2 : d2, g, R.Tq[r]);
+      }
+    }
+  }
+}
+
+template <bool kVarying, bool kGrad, int kMode>
+__global__ void __launch_bounds__(kThreads, HK_MIN_BLOCKS) pair_kernel(const PairParams P) {
+  __shared__ __align__(128) double s_buf[2][kSlots * kBJ];
+  __shared__ __align__(8) uint64_t s_bar[2];
+
+  const int tid = threadIdx.x;
+  const Item it = P.items[blockIdx.x];
+  load_exp2_table();
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    mbar_fence_init();
+  }
+
+  BlockInfo bi;
+  bi.rb = it.rb;
+  bi.re = it.re;
+  bi.lbmin = P.d.lb[it.rb];
+  bi.ubmax = P.d.ub[it.re - 1];
+  bi.t_first = P.d.t[it.rb];
+  bi.t_last = P.d.t[it.re - 1];
+
+  RowState R;
+  bool valid[kRowsPerThread];
+#pragma unroll
+  for (int r = 0; r < kRowsPerThread; ++r) {
+    int row = it.rb + tid + r * kThreads;
+    valid[r] = row < it.re;
+    row = valid[r] ? row : it.re - 1;
+    R.t[r] = P.d.t[row];
+    R.x[r] = P.d.x[row];
+    R.y[r] = P.d.y[row];
+    R.lb[r] = P.d.lb[row];
+    R.ub[r] = P.d.ub[row];
+    R.B[r] = R.B2[r] = R.T[r] = R.Td[r] = R.Tq[r] = 0.0;
+  }
+  __syncthreads();
+
+  auto next_live = [&](int J) {
+    while (J < it.te && tile_type(J, bi, P) == kSkip) ++J;
+    return J;
+  };
+
+  int cur = next_live(it.tb);
+  int stage = 0;
+  unsigned phases = 0u;  // bit s = parity of the next wait on stage s
+  if (cur < it.te && tid == 0)
+    issue_tile<kVarying, kGrad>(tile_type(cur, bi, P), cur, s_buf[0], &s_bar[0], P);
+  while (cur < it.te) {
+    const int nxt = next_live(cur + 1);
+    if (nxt < it.te && tid == 0)
+      issue_tile<kVarying, kGrad>(tile_type(nxt, bi, P), nxt, s_buf[stage ^ 1], &s_bar[stage ^ 1],
+                                  P);
+    mbar_wait(&s_bar[stage], (phases >> stage) & 1u);
+    phases ^= 1u << stage;
+    const double* buf = s_buf[stage];
+    switch (tile_type(cur, bi, P)) {
+      case kTileBT:
+        tile_fast<kVarying, kGrad, kMode, true, true>(R, buf, P.c);
+        break;
+      case kTileB:
+        tile_fast<kVarying, kGrad, kMode, true, false>(R, buf, P.c);
+        break;
+      case kTileT:
+        tile_fast<kVarying, kGrad, kMode, false, true>(R, buf, P.c);
+        break;
+      default:
+        tile_masked<kVarying, kGrad, kMode>(R, cur * kBJ, P.d.n, buf, P.c);
+        break;
+    }
+    __syncthreads();  // every warp is done with this stage before it is refilled
+    cur = nxt;
+    stage ^= 1;
+  }
+
+  const size_t plane = static_cast<size_t>(P.rows_total);
+  double* out = P.partial + static_cast<size_t>(it.slot) * 5 * plane;
+#pragma unroll
+  for (int r = 0; r < kRowsPerThread; ++r) {
+    if (!valid[r]) continue;
+    const size_t i = static_cast<size_t>(it.rb + tid + r * kThreads - P.rows_base);
+    out[0 * plane + i] = R.B[r];
+    out[1 * plane + i] = R.B2[r];
+    out[2 * plane + i] = R.T[r];
+    out[3 * plane + i] = R.Td[r];
+    out[4 * plane + i] = R.Tq[r];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// prep
+
+__global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= d.npad) return;
+  if (j < d.n) {
+    const double q = c.varying ? d.q[j] : 1.0;
+    const double K = -(c.half_s2 * q) * kLog2e16;
+    const int jr = min(d.n, (j / kBJ + 1) * kBJ) - 1;
+    const double dtr = d.t[jr] - d.t[j];
+    const double w = q * exp(-c.omega * dtr);
+    d.K[j] = K;
+    d.thr[j] = kFlushArg / (-K);
+    d.w[j] = w;
+    d.v[j] = dtr * w;
+    d.z[j] = q * w;
+  } else {
+    d.K[j] = -1.0;
+    d.thr[j] = 0.0;
+    d.w[j] = 0.0;
+    d.v[j] = 0.0;
+    d.z[j] = 0.0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// finish + reduce
+
+constexpr int kFinishThreads = 256;
+
+__device__ __forceinline__ double gaussian_cdf(double z) {
+  return 0.5 * erfc(-z * 0.7071067811865475244);  // model.hpp:157-160
+}
+
+__device__ __forceinline__ double gaussian_pdf(double z) {
+  return kInvSqrt2Pi * exp(-0.5 * z * z);  // model.hpp:152-155
+}
+
+__global__ void __launch_bounds__(kFinishThreads) finish_kernel(
+    const DeviceCatalog d, const EvalCoef c, const double* __restrict__ partial, int slots,
+    int rows_base, int rows_total, int with_grad, double* ell_rows, double* grad_rows,
+    double* blockpart) {
+  __shared__ double s_red[6][kFinishThreads];
+  const int tid = threadIdx.x;
+  const int li = blockIdx.x * kFinishThreads + tid;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  if (li < rows_total) {
+    const size_t plane = static_cast<size_t>(rows_total);
+    double B = 0, B2 = 0, T = 0, Td = 0, Tq = 0;
+    for (int s = 0; s < slots; ++s) {
+      const double* p = partial + static_cast<size_t>(s) * 5 * plane + li;
+      B += p[0];
+      B2 += p[plane];
+      T += p[2 * plane];
+      Td += p[3 * plane];
+      Tq += p[4 * plane];
+    }
+    const double ti = d.t[rows_base + li];
+    const double S = c.a * B + c.c * T;
+    const double lg = log(fmax(S, kRateClip));  // == combine_lanes, model.hpp:311-326
+    // integral_term, model.hpp:301-306
+    const double r = c.t_end - ti;
+    const double Phi_r = gaussian_cdf(r / c.tau_t);
+    const double Phi_0 = gaussian_cdf(-ti / c.tau_t);
+    const double er = exp(-r / c.sigma_t);
+    const double Lam = c.mu0 * (Phi_r - Phi_0) + (-c.xi0 * (er - 1.0));
+    acc[0] = lg - Lam;
+    if (with_grad) {
+      const double inv = S >= kRateClip ? 1.0 / S : 0.0;
+      const double tau = c.tau_t, om = c.omega;
+      acc[1] = (c.a * B / c.mu0) * inv - (Phi_r - Phi_0);
+      acc[2] = (c.a * (B2 / (tau * tau) - B) / tau) * inv +
+               c.mu0 * (gaussian_pdf(r / tau) * r + gaussian_pdf(ti / tau) * ti) / (tau * tau);
+      acc[3] = (c.c * T / c.xi0) * inv - (1.0 - er);
+      acc[4] = (c.c * (2.0 * c.half_s2 * Tq - 2.0 * T) / c.sigma_x) * inv;
+      acc[5] = -om * om * ((c.c * T / om - c.c * Td) * inv - c.xi0 * r * er);
+    }
+    if (ell_rows) ell_rows[li] = acc[0];
+    if (grad_rows)
+      for (int k = 0; k < 5; ++k) grad_rows[static_cast<size_t>(li) * 5 + k] = acc[1 + k];
+  }
+#pragma unroll
+  for (int k = 0; k < 6; ++k) s_red[k][tid] = acc[k];
+  __syncthreads();
+  for (int h = kFinishThreads / 2; h > 0; h >>= 1) {
+    if (tid < h)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s_red[k][tid] += s_red[k][tid + h];
+    __syncthreads();
+  }
+  if (tid < 6) blockpart[static_cast<size_t>(blockIdx.x) * 6 + tid] = s_red[tid][0];
+}
+
+__global__ void __launch_bounds__(kFinishThreads) reduce_kernel(const double* __restrict__ blockpart,
+                                                                int n_blocks, double* out6) {
+  __shared__ double s_red[6][kFinishThreads];
+  const int tid = threadIdx.x;
+  double acc[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = tid; b < n_blocks; b += kFinishThreads)
+#pragma unroll
+    for (int k = 0; k < 6; ++k) acc[k] += blockpart[static_cast<size_t>(b) * 6 + k];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) s_red[k][tid] = acc[k];
+  __syncthreads();
+  for (int h = kFinishThreads / 2; h > 0; h >>= 1) {
+    if (tid < h)
+#pragma unroll
+      for (int k = 0; k < 6; ++k) s_red[k][tid] += s_red[k][tid + h];
+    __syncthreads();
+  }
+  if (tid < 6) out6[tid] = s_red[tid][0];
+}
+
+// ---------------------------------------------------------------------------
+// FP64 peak probe: 8 independent DFMA chains per thread, register resident.
+
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double* sink, int iters, double s) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-3, a2 = a0 + 2e-3, a3 = a0 + 3e-3;
+  double a4 = a0 + 4e-3, a5 = a0 + 5e-3, a6 = a0 + 6e-3, a7 = a0 + 7e-3;
+  const double m = 0.999999, k = s;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, m, k);
+      a1 = fma(a1, m, k);
+      a2 = fma(a2, m, k);
+      a3 = fma(a3, m, k);
+      a4 = fma(a4, m, k);
+      a5 = fma(a5, m, k);
+      a6 = fma(a6, m, k);
+      a7 = fma(a7, m, k);
+    }
+  }
+  const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (r == 12345.678) sink[threadIdx.x] = r;
+}
+
+template <bool V, bool G, int M>
+void launch_pair_t(const PairParams& P, int n_items, cudaStream_t s) {
+  pair_kernel<V, G, M><<<n_items, kThreads, 0, s>>>(P);
+}
+
+}  // namespace
+
+void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
+  const int threads = 256;
+  prep_kernel<<<(d.npad + threads - 1) / threads, threads, 0, s>>>(d, c);
+}
+
+void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
+                 double* partial, int rows_base, int rows_total, bool with_grad, cudaStream_t s) {
+  if (n_items <= 0) return;
+  PairParams P{d, c, items, partial, rows_base, rows_total};
+  const int key = (c.varying ? 6 : 0) + (with_grad ? 3 : 0) + c.mode;
+  switch (key) {
+    case 0: launch_pair_t<false, false, kExact>(P, n_items, s); break;
+    case 1: launch_pair_t<false, false, kFlush>(P, n_items, s); break;
+    case 2: launch_pair_t<false, false, kChecked>(P, n_items, s); break;
+    case 3: launch_pair_t<false, true, kExact>(P, n_items, s); break;
+    case 4: launch_pair_t<false, true, kFlush>(P, n_items, s); break;
+    case 5: launch_pair_t<false, true, kChecked>(P, n_items, s); break;
+    case 6: launch_pair_t<true, false, kExact>(P, n_items, s); break;
+    case 7: launch_pair_t<true, false, kFlush>(P, n_items, s); break;
+    case 8: launch_pair_t<true, false, kChecked>(P, n_items, s); break;
+    case 9: launch_pair_t<true, true, kExact>(P, n_items, s); break;
+    case 10: launch_pair_t<true, true, kFlush>(P, n_items, s); break;
+    default: launch_pair_t<true, true, kChecked>(P, n_items, s); break;
+  }
+}
+
+int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* partial, int slots,
+                  int rows_base, int rows_total, bool with_grad, double* ell_rows,
+                  double* grad_rows, double* blockpart, cudaStream_t s) {
+  const int blocks = (rows_total + kFinishThreads - 1) / kFinishThreads;
+  finish_kernel<<<blocks, kFinishThreads, 0, s>>>(d, c, partial, slots, rows_base, rows_total,
+                                                   with_grad ? 1 : 0, ell_rows, grad_rows,
+                                                   blockpart);
+  return blocks;
+}
+
+void launch_reduce(const double* blockpart, int n_blocks, double* out6, cudaStream_t s) {
+  reduce_kernel<<<1, kFinishThreads, 0, s>>>(blockpart, n_blocks, out6);
+}
+
+double measure_fp64_peak(int device, double* ms_out) {
+  cudaSetDevice(device);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  double* sink = nullptr;
+  cudaMalloc(&sink, 256 * sizeof(double));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_probe_kernel<<<blocks, threads>>>(sink, 64, 1e-7);  // warm-up
+  cudaEventRecord(e0);
+  dfma_probe_kernel<<<blocks, threads>>>(sink, iters, 1e-7);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (ms_out) *ms_out = ms;
+  const double fmas = static_cast<double>(blocks) * threads * iters * 16.0 * 8.0;
+  return 2.0 * fmas / (ms * 1e-3) / 1e12;
+}
+
+}  // namespace hk

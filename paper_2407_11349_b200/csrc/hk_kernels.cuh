@@ -1,0 +1,61 @@
+// Launch-side view of the device kernels (shared by hk_kernels.cu and the
+// context code in hk_capi.cu).  Plain structs only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace hk {
+
+// One work item = one CTA: rows [rb, re) (<= kBI rows) against column tiles
+// [tb, te); its five per-row partial sums land in partial slot `slot`.
+struct Item {
+  int rb, re, tb, te, slot, pad;
+};
+
+// Per-evaluation coefficients, all derived on the host in double exactly
+// once (HawkesParams accessors, types.hpp:105-109; coefficients,
+// model.hpp:328-336).
+struct EvalCoef {
+  double mu0, tau_t, xi0, sigma_x, sigma_t;
+  double tau_prec, sx_prec, omega;
+  double a;       // background_coefficient<double>
+  double c;       // trigger_coefficient<double>
+  double half_s2; // 0.5 * sx_prec * sx_prec (model.hpp:277)
+  double Kb;      // -0.5 tau_prec^2 * 16/ln2   (background exponent per td^2)
+  double Kq0;     // -half_s2 * 16/ln2           (trigger exponent per d^2, q = 1)
+  double Kw;      // -omega * 16/ln2             (trigger exponent per td)
+  double t_end;   // t[N-1]
+  int varying;
+  int mode;       // ExpMode: kExact / kFlush / kChecked from the argument bound
+};
+
+struct DeviceCatalog {
+  int n, npad;
+  const double* t;   // [npad], padded with t[n-1]
+  const double* x;   // [npad], padded with 0
+  const double* y;   // [npad]
+  const double* q;   // density, [npad], padded with 1
+  const int* lb;     // [n] count_before(t_i) (model.hpp:241-243)
+  const int* ub;     // [n] upper_bound(t_i)
+  double* K;         // prep: per-source trigger exponent coefficient  [npad]
+  double* thr;       // prep: d^2 beyond which the spatial factor flushes [npad]
+  double* w;         // prep: q_j exp(-omega (t_ref(J) - t_j))        [npad]
+  double* v;         // prep: (t_ref(J) - t_j) w_j                    [npad]
+  double* z;         // prep: q_j w_j                                 [npad]
+};
+
+void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
+void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
+                 double* partial, int rows_base, int rows_total, bool with_grad, cudaStream_t s);
+// Combines the partial slots per row, forms ell_n and its gradient, and
+// reduces to one 6-vector per block; writes per-row outputs for rows in
+// [out_b, out_e) when the pointers are non-null.
+int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* partial, int slots,
+                  int rows_base, int rows_total, bool with_grad, double* ell_rows,
+                  double* grad_rows, double* blockpart, cudaStream_t s);
+void launch_reduce(const double* blockpart, int n_blocks, double* out6, cudaStream_t s);
+double measure_fp64_peak(int device, double* ms);
+
+}  // namespace hk

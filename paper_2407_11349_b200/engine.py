@@ -1,0 +1,307 @@
+"""Host-side mirror of the reference's hot-path interface
+(/root/reference/proj/include/hawkes/{types,model,engine}.hpp), backed by
+the B200 engine through the C ABI.
+
+Names, argument meaning and error behaviour follow the reference:
+
+  reference (C++)                               here
+  -------------------------------------------------------------------------
+  Variant, Precision           types.hpp:16,112  Variant, Precision
+  Catalog / Catalog::sorted    types.hpp:41-78   Catalog / Catalog.sorted
+  HawkesParams + validate      types.hpp:83-110  HawkesParams
+  Partition::make              engine.hpp:22-43  Partition.make / make_partition
+  log_likelihood               engine.hpp:101-110 log_likelihood
+  event_contribution           model.hpp:351-356 event_contribution
+  LikelihoodWorkspace<double>  engine.hpp:117-229 LikelihoodWorkspace
+  benchmark_catalog            engine.hpp:251-259 benchmark_catalog
+  (new)                                          log_likelihood_and_gradient
+
+std::invalid_argument maps to ValueError, std::out_of_range to IndexError.
+Precision.single is rejected with ValueError: the GPU path is FP64 and there
+is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import weakref
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+
+class Variant(enum.IntEnum):
+    constant = 0
+    varying = 1
+
+
+class Precision(enum.Enum):
+    single = "single"
+    dbl = "double"
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Catalog:
+    """Immutable, time-ordered event set in SoA form (t in weeks, lon/lat in
+    degrees, density per square mile).  Validation and messages are the
+    reference's (types.hpp:43-57)."""
+
+    __slots__ = ("t", "lon", "lat", "density", "_ctx", "__weakref__")
+
+    def __init__(self, t, lon, lat, density=None):
+        t = _f64(t)
+        lon = _f64(lon)
+        lat = _f64(lat)
+        density = np.ones_like(t) if density is None else _f64(density)
+        if not (len(t) == len(lon) == len(lat) == len(density)):
+            raise ValueError("Catalog: column lengths differ")
+        check(lib.hk_validate_catalog(t, lon, lat, density, len(t)))
+        for a in (t, lon, lat, density):
+            a.setflags(write=False)
+        self.t, self.lon, self.lat, self.density = t, lon, lat, density
+        self._ctx = None
+
+    @classmethod
+    def sorted(cls, t, lon, lat, density=None) -> "Catalog":
+        t = _f64(t)
+        order = np.argsort(t, kind="stable")
+        dens = np.ones_like(t) if density is None else _f64(density)
+        return cls(t[order], _f64(lon)[order], _f64(lat)[order], dens[order])
+
+    def size(self) -> int:
+        return len(self.t)
+
+    __len__ = size
+
+    def t_end(self) -> float:
+        return float(self.t[-1])
+
+    def arrays(self):
+        return self.t, self.lon, self.lat, self.density
+
+
+@dataclass(frozen=True)
+class HawkesParams:
+    mu0: float = 1.0
+    tau_t: float = 1.0
+    xi0: float = 1.0
+    sigma_x: float = 1.0
+    sigma_t: float = 1.0
+    area: float = 1.0
+    variant: Variant = Variant.constant
+
+    def validate(self) -> None:
+        p = self.to_c()
+        check(lib.hk_validate_params(C.byref(p)))
+
+    def to_c(self) -> _lib.hk_params:
+        return _lib.hk_params(float(self.mu0), float(self.tau_t), float(self.xi0),
+                              float(self.sigma_x), float(self.sigma_t), float(self.area),
+                              int(self.variant))
+
+    def sigma_x_prec(self) -> float:
+        return 1.0 / self.sigma_x
+
+    def tau_t_prec(self) -> float:
+        return 1.0 / self.tau_t
+
+    def omega(self) -> float:
+        return 1.0 / self.sigma_t
+
+    def inv_area(self) -> float:
+        return 1.0 / self.area
+
+    def with_(self, **kw) -> "HawkesParams":
+        return replace(self, **kw)
+
+
+class Partition:
+    """Contiguous row ranges (engine.hpp:22-43).  The GPU engine keeps the
+    type for API compatibility; it shards rows by its own cost model and the
+    result does not depend on the partition beyond rounding."""
+
+    def __init__(self, ranges):
+        self.ranges = [(int(b), int(e)) for b, e in ranges]
+
+    def workers(self) -> int:
+        return len(self.ranges)
+
+    @staticmethod
+    def make(n: int, g: int) -> "Partition":
+        if n < 0 or g < 0:
+            raise ValueError("Partition: sizes must be non-negative")
+        b = np.zeros(g + 1, dtype=np.uintp)
+        check(lib.hk_partition_make(n, g, b))
+        return Partition(zip(b[:-1], b[1:]))
+
+
+def make_partition(n: int, g: int) -> Partition:
+    return Partition.make(n, g)
+
+
+def plan_shards(t, g: int) -> np.ndarray:
+    """Cost-balanced row-shard boundaries (g+1) for g devices/ranks."""
+    t = _f64(t)
+    b = np.zeros(g + 1, dtype=np.uintp)
+    check(lib.hk_plan_shards(t, len(t), g, b))
+    return b.astype(np.int64)
+
+
+def benchmark_catalog(n: int, seed: int = 42) -> Catalog:
+    """The reference's synthetic uniform catalog (engine.hpp:251-259),
+    bit-identical to its mt19937_64 / libstdc++ draws."""
+    t, x, y, d = (np.zeros(n) for _ in range(4))
+    check(lib.hk_benchmark_catalog(n, seed, t, x, y, d))
+    return Catalog(t, x, y, d)
+
+
+class Evaluator:
+    """One engine context: the catalog resident on `n_gpus` devices (or one
+    rank's row shard on `device`)."""
+
+    def __init__(self, catalog: Catalog, n_gpus: int = 1, shard=None, device: int = 0):
+        self.catalog = catalog
+        h = C.c_void_p()
+        t, x, y, d = catalog.arrays()
+        if shard is None:
+            check(lib.hk_create(t, x, y, d, len(t), n_gpus, C.byref(h)))
+        else:
+            b, e = shard
+            check(lib.hk_create_shard(t, x, y, d, len(t), b, e, device, C.byref(h)))
+        self._h = h
+        self._fin = weakref.finalize(self, lib.hk_destroy, h)
+
+    def close(self) -> None:
+        self._fin()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def rows(self):
+        b, e, nd = C.c_size_t(), C.c_size_t(), C.c_int()
+        check(lib.hk_rows(self._h, C.byref(b), C.byref(e), C.byref(nd)))
+        return b.value, e.value, nd.value
+
+    def set_locations(self, lon, lat) -> None:
+        lon, lat = _f64(lon), _f64(lat)
+        if len(lon) != len(self.catalog) or len(lat) != len(self.catalog):
+            raise ValueError("set_locations: length mismatch")
+        check(lib.hk_set_locations(self._h, lon, lat))
+
+    def set_locations_device(self, lon_ptr: int, lat_ptr: int) -> None:
+        check(lib.hk_set_locations_device(self._h, C.c_void_p(lon_ptr), C.c_void_p(lat_ptr)))
+
+    def eval(self, params: HawkesParams, grad: bool = False):
+        p = params.to_c()
+        ll = C.c_double()
+        g = np.zeros(5)
+        check(lib.hk_eval(self._h, C.byref(p), C.byref(ll),
+                          g.ctypes.data_as(C.c_void_p) if grad else None))
+        return (ll.value, g) if grad else ll.value
+
+    def eval_async(self, params: HawkesParams, grad: bool = True) -> None:
+        p = params.to_c()
+        check(lib.hk_eval_async(self._h, C.byref(p), int(grad)))
+
+    def result_device_ptr(self) -> int:
+        return lib.hk_result_device(self._h)
+
+    def stream_ptr(self, dev: int = 0) -> int:
+        return lib.hk_stream(self._h, dev)
+
+    def eval_rows(self, params: HawkesParams, b: int, e: int, grad: bool = False):
+        if b < 0 or e < 0:
+            raise IndexError("event_contribution: index out of range")
+        p = params.to_c()
+        ell = np.zeros(max(e - b, 1))
+        g = np.zeros((max(e - b, 1), 5))
+        check(lib.hk_eval_rows(self._h, C.byref(p), b, e, ell,
+                               g.ctypes.data_as(C.c_void_p) if grad else None))
+        return (ell, g) if grad else ell
+
+    def set_profiling(self, on: bool) -> None:
+        check(lib.hk_set_profiling(self._h, int(on)))
+
+    def profile(self):
+        ms, npair, ntot = C.c_double(), C.c_long(), C.c_long()
+        check(lib.hk_profile(self._h, C.byref(ms), C.byref(npair), C.byref(ntot)))
+        return ms.value, npair.value, ntot.value
+
+    def reset_profile(self) -> None:
+        check(lib.hk_reset_profile(self._h))
+
+
+def _evaluator_for(catalog: Catalog) -> Evaluator:
+    # One cached single-device context per catalog (the catalog is immutable).
+    if catalog._ctx is None:
+        catalog._ctx = Evaluator(catalog)
+    return catalog._ctx
+
+
+def _check_call(catalog: Catalog, p: HawkesParams, part: Partition, precision: Precision):
+    p.validate()
+    if not part.ranges or part.ranges[-1][1] != catalog.size():
+        raise ValueError("log_likelihood: partition does not cover the catalog")
+    if precision != Precision.dbl:
+        raise ValueError("log_likelihood: the B200 engine evaluates in double precision only "
+                         "(Precision::single is not implemented on the GPU path)")
+
+
+def log_likelihood(catalog: Catalog, p: HawkesParams, part: Partition,
+                   precision: Precision = Precision.dbl) -> float:
+    """engine.hpp:101-110 on the B200 engine."""
+    _check_call(catalog, p, part, precision)
+    return _evaluator_for(catalog).eval(p)
+
+
+def log_likelihood_and_gradient(catalog: Catalog, p: HawkesParams, part: Partition | None = None,
+                                precision: Precision = Precision.dbl):
+    """(log-likelihood, d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t))."""
+    _check_call(catalog, p, part or Partition.make(catalog.size(), 1), precision)
+    return _evaluator_for(catalog).eval(p, grad=True)
+
+
+def event_contribution(p: HawkesParams, catalog: Catalog, n: int) -> float:
+    """model.hpp:351-356."""
+    if n < 0 or n >= catalog.size():
+        raise IndexError("event_contribution: index out of range")
+    p.validate()
+    return float(_evaluator_for(catalog).eval_rows(p, n, n + 1)[0])
+
+
+class LikelihoodWorkspace:
+    """LikelihoodWorkspace<double> (engine.hpp:117-229) on the engine: same
+    methods and semantics (proposal evaluated, promoted on commit), every
+    evaluation a full device pass."""
+
+    def __init__(self, catalog: Catalog, variant: Variant, workers: int = 1):
+        self._catalog = catalog
+        self._variant = Variant(variant)
+        self._ev = Evaluator(catalog)
+        self._proposal = None
+        self._current = None
+
+    def evaluate_full(self, p: HawkesParams) -> float:
+        p = replace(p, variant=self._variant)
+        self._current = p
+        return self._ev.eval(p)
+
+    def evaluate_proposal(self, p: HawkesParams) -> float:
+        p = replace(p, variant=self._variant)
+        self._proposal = p
+        return self._ev.eval(p)
+
+    def commit_proposal(self) -> None:
+        if self._proposal is not None:
+            self._current = self._proposal
+        self._proposal = None
+
+    def set_locations(self, lon, lat) -> None:
+        self._ev.set_locations(lon, lat)

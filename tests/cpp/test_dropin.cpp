@@ -1,0 +1,219 @@
+// Drop-in gate: the reference's own test logic (test_engine.cpp,
+// test_model.cpp, acceptance.cpp criterion 1) and its MH Sampler (mcmc.hpp),
+// run against the B200 engine through include/hawkes_b200/engine.hpp, with
+// the reference's CPU implementation (compiled from the same headers) as the
+// checker.  One PASS/FAIL line per check, exit status = number of failures
+// (acceptance.cpp convention).  Built where /root/reference exists
+// (oracle/Makefile `dropin`), run on a GPU box (tests/test_dropin.py).
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "hawkes/engine.hpp"
+#include "hawkes/mcmc.hpp"
+#include "hawkes/simulate.hpp"
+#include "hawkes_b200/engine.hpp"
+
+using namespace hawkes;
+
+namespace dropin {
+ChainOutput fixed_chain_b200(const ChainConfig& config, const Catalog& catalog);
+ChainOutput cut_chain_b200(const ChainConfig& config, const Catalog& catalog, const RegionTable& regions);
+}  // namespace dropin
+
+namespace {
+
+int failures = 0;
+
+void report(const std::string& what, bool pass, const std::string& detail) {
+  std::printf("%s: %s (%s)\n", pass ? "PASS" : "FAIL", what.c_str(), detail.c_str());
+  std::fflush(stdout);
+  if (!pass) ++failures;
+}
+
+Catalog random_catalog(std::mt19937_64& rng, std::size_t n) {  // test_engine.cpp:19-27
+  std::uniform_real_distribution<double> ut(0.0, 80.0), ux(-4.0, 4.0), ud(0.5, 3000.0);
+  std::vector<Event> events;
+  for (std::size_t i = 0; i < n; ++i) events.push_back({ut(rng), ux(rng), ux(rng), "", ud(rng)});
+  return Catalog::sorted(std::move(events));
+}
+
+HawkesParams random_params(std::mt19937_64& rng) {  // test_engine.cpp:29-38
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  HawkesParams p;
+  p.mu0 = 0.05 + 2.0 * u(rng);
+  p.tau_t = 0.5 + 10.0 * u(rng);
+  p.xi0 = 0.05 + 1.5 * u(rng);
+  p.sigma_x = 0.05 + u(rng);
+  p.sigma_t = 0.2 + 5.0 * u(rng);
+  p.area = 10.0 + 100.0 * u(rng);
+  return p;
+}
+
+void engine_agrees_with_naive() {  // test_engine.cpp:127-141
+  std::mt19937_64 rng(53);
+  double worst = 0.0;
+  for (int rep = 0; rep < 10; ++rep) {
+    const std::size_t n = 10 + rng() % 800;
+    const Catalog catalog = random_catalog(rng, n);
+    HawkesParams p = random_params(rng);
+    if (rep % 2) p.variant = Variant::varying;
+    const double oracle = naive_log_likelihood(catalog, p);
+    const double got = b200::log_likelihood(catalog, p, make_partition(n, 1 + rep % 4), Precision::dbl);
+    worst = std::max(worst, std::abs(got - oracle) / std::abs(oracle));
+  }
+  char d[96];
+  std::snprintf(d, sizeof d, "max rel err %.3g (tol 1e-10)", worst);
+  report("engine agrees with the naive oracle (test_engine.cpp:127-141)", worst <= 1e-10, d);
+}
+
+void criterion_1_subset() {  // acceptance.cpp:50-84, 20 of its 100 catalogs
+  std::mt19937_64 rng(101);
+  std::uniform_int_distribution<std::size_t> un(10, 5000);
+  std::uniform_real_distribution<double> umu(0.1, 2.0), utau(0.5, 20.0), uxi(0.05, 0.9), usx(0.02, 0.5),
+      ust(0.2, 10.0);
+  double worst = 0.0;
+  for (int c = 0; c < 20; ++c) {
+    const std::size_t n = un(rng);
+    std::vector<Event> events = benchmark_catalog(n, 9000 + static_cast<std::uint64_t>(c)).events();
+    for (Event& e : events) {
+      e.t = static_cast<float>(e.t);
+      e.lon = static_cast<float>(e.lon);
+      e.lat = static_cast<float>(e.lat);
+    }
+    const Catalog catalog(std::move(events));
+    HawkesParams p;
+    p.mu0 = umu(rng);
+    p.tau_t = utau(rng);
+    p.xi0 = uxi(rng);
+    p.sigma_x = usx(rng);
+    p.sigma_t = ust(rng);
+    p.area = domain_area(catalog);
+    p.variant = c % 2 == 0 ? Variant::constant : Variant::varying;
+    const double reference = naive_log_likelihood(catalog, p);
+    for (std::size_t g : {1, 2, 4, 8}) {
+      const double d = b200::log_likelihood(catalog, p, make_partition(n, g), Precision::dbl);
+      worst = std::max(worst, std::abs(d - reference) / std::abs(reference));
+    }
+  }
+  char d[96];
+  std::snprintf(d, sizeof d, "max rel err %.3g (tol 1e-10)", worst);
+  report("criterion 1 catalogs vs naive_log_likelihood (acceptance.cpp:50-84)", worst <= 1e-10, d);
+}
+
+void contributions_and_errors() {
+  std::mt19937_64 rng(23);  // test_model.cpp:196-218
+  double worst = 0.0;
+  for (int rep = 0; rep < 10; ++rep) {
+    HawkesParams q = random_params(rng);
+    if (rep % 2) q.variant = Variant::varying;
+    const Catalog catalog = random_catalog(rng, 40);
+    for (std::size_t n = 0; n < catalog.size(); n += 7)
+      worst = std::max(worst, std::abs(b200::event_contribution(q, catalog, n) -
+                                       event_contribution(q, catalog, n)) /
+                                  std::max(1.0, std::abs(event_contribution(q, catalog, n))));
+  }
+  char d[96];
+  std::snprintf(d, sizeof d, "max err %.3g (tol 1e-12)", worst);
+  report("event_contribution vs the reference (test_model.cpp:196-218)", worst <= 1e-12, d);
+
+  const Catalog catalog = random_catalog(rng, 50);
+  HawkesParams bad;
+  bad.sigma_t = 0.0;
+  bool ok = false;
+  try {
+    b200::log_likelihood(catalog, bad, make_partition(50, 1), Precision::dbl);
+  } catch (const std::invalid_argument& e) {
+    ok = std::string(e.what()).find("sigma_t must be positive") != std::string::npos;
+  }
+  bool ok2 = false;
+  try {
+    b200::log_likelihood(catalog, HawkesParams{}, make_partition(49, 1), Precision::dbl);
+  } catch (const std::invalid_argument& e) {
+    ok2 = std::string(e.what()) == "log_likelihood: partition does not cover the catalog";
+  }
+  bool ok3 = false;
+  try {
+    b200::event_contribution(HawkesParams{}, catalog, 50);
+  } catch (const std::out_of_range&) {
+    ok3 = true;
+  }
+  report("exception types and messages (types.hpp:92-103, engine.hpp:104-105, model.hpp:352)",
+         ok && ok2 && ok3, "invalid_argument / out_of_range");
+}
+
+void gradient_vs_fd() {
+  std::mt19937_64 rng(7);
+  const Catalog catalog = random_catalog(rng, 400);
+  HawkesParams p = random_params(rng);
+  p.variant = Variant::varying;
+  std::array<double, 5> g{};
+  b200::log_likelihood_and_gradient(catalog, p, make_partition(400, 1), g);
+  double worst = 0.0;
+  for (int k = 0; k < 5; ++k) {
+    auto f = [&](double h) {
+      HawkesParams a = p, b = p;
+      double* pa[5] = {&a.mu0, &a.tau_t, &a.xi0, &a.sigma_x, &a.sigma_t};
+      double* pb[5] = {&b.mu0, &b.tau_t, &b.xi0, &b.sigma_x, &b.sigma_t};
+      *pa[k] += h;
+      *pb[k] -= h;
+      return (log_likelihood(catalog, a, make_partition(400, 1), Precision::dbl) -
+              log_likelihood(catalog, b, make_partition(400, 1), Precision::dbl)) / (2 * h);
+    };
+    const double* pv[5] = {&p.mu0, &p.tau_t, &p.xi0, &p.sigma_x, &p.sigma_t};
+    const double h = 2e-3 * *pv[k];
+    const double r1 = (4 * f(h / 2) - f(h)) / 3, r2 = (4 * f(h / 4) - f(h / 2)) / 3;
+    const double fd = (16 * r2 - r1) / 15;
+    worst = std::max(worst, std::abs(g[k] - fd) / std::max(1.0, std::abs(fd)));
+  }
+  char d[96];
+  std::snprintf(d, sizeof d, "max err vs Richardson FD of the reference LL %.3g (tol 1e-6)", worst);
+  report("gradient vs finite differences of the reference log_likelihood", worst <= 1e-6, d);
+}
+
+void sampler_unchanged() {
+  // the reference's own Sampler (mcmc.hpp) with the GPU workspace vs the CPU one
+  SimConfig sim;
+  sim.immigrant_rate = 3.0;
+  sim.horizon = 100.0;
+  sim.seed = 606;
+  const Catalog catalog = simulate_catalog(sim);
+  ChainConfig config;
+  config.iterations = 40;
+  config.burn_in = 10;
+  config.seed = 42;
+  config.initial.mu0 = 0.5;
+  config.initial.tau_t = 5.0;
+  config.initial.xi0 = 0.5;
+  config.initial.sigma_x = 0.1;
+  config.initial.sigma_t = 2.0;
+  config.initial.area = domain_area(catalog);
+  const ChainOutput cpu = run_fixed_posterior(config, catalog);
+  const ChainOutput gpu = dropin::fixed_chain_b200(config, catalog);
+  bool same = cpu.draws.size() == gpu.draws.size() && cpu.accepts == gpu.accepts;
+  double worst = 0.0;
+  for (std::size_t i = 0; same && i < cpu.draws.size(); ++i) {
+    for (std::size_t k = 0; k < kParamCount; ++k) same = same && cpu.draws[i][k] == gpu.draws[i][k];
+    worst = std::max(worst, std::abs(cpu.loglik_trace[i] - gpu.loglik_trace[i]) / std::abs(cpu.loglik_trace[i]));
+  }
+  char d[128];
+  std::snprintf(d, sizeof d, "N=%zu, %zu draws identical: %s, loglik trace max rel err %.3g", catalog.size(),
+                cpu.draws.size(), same ? "yes" : "no", worst);
+  report("mcmc.hpp Sampler unchanged on the B200 workspace: same chain as the CPU workspace",
+         same && worst <= 1e-10, d);
+}
+
+}  // namespace
+
+int main() {
+  engine_agrees_with_naive();
+  criterion_1_subset();
+  contributions_and_errors();
+  gradient_vs_fd();
+  sampler_unchanged();
+  std::printf("%d failure(s)\n", failures);
+  return failures;
+}

@@ -1,0 +1,299 @@
+"""GPU parity: the B200 engine (through the C ABI) against the oracle and the
+reference's golden vectors.  Gate: 1e-10 relative on the log-likelihood;
+1e-10 on every gradient component relative to max(|g_ref|, sum_n |d ell_n/d
+theta|) (the conditioning-aware scale of SURVEY.md section 7), with the
+plain relative error reported alongside.  Integer/index work (catalog,
+partitions, shard plans) is bit-exact and tested in test_oracle.py."""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import float_round, golden, golden_catalog
+
+pytestmark = pytest.mark.gpu
+
+LL_TOL = 1e-10
+GRAD_TOL = 1e-10
+BENCH = dict(mu0=1.0, tau_t=5.0, xi0=0.5, sigma_x=0.5, sigma_t=2.0, area=100.0)  # engine.hpp:272-273
+
+
+@pytest.fixture(scope="module")
+def eng(cuda_device):
+    import paper_2407_11349_b200 as eng
+    return eng
+
+
+def hp(eng, p, variant):
+    return eng.HawkesParams(**{k: p[k] for k in ("mu0", "tau_t", "xi0", "sigma_x", "sigma_t", "area")},
+                            variant=eng.Variant(variant))
+
+
+def check_grad(g, g_ref, scale, tol=GRAD_TOL):
+    den = np.maximum(np.abs(g_ref), scale)
+    diff = np.abs(g - g_ref)
+    err = np.where(den > 0, diff / np.where(den > 0, den, 1.0), diff)  # 0/0: both exactly zero
+    assert np.all(err <= tol), (err, g, g_ref)
+
+
+def run_vs_oracle(eng, oracle, cat, p, variant, grad=True):
+    ev = eng.Evaluator(eng.Catalog(*cat))
+    ll, g = ev.eval(hp(eng, p, variant), grad=True)
+    ll_ref, g_ref = oracle.ll_grad(cat, p, variant)
+    assert abs(ll - ll_ref) <= LL_TOL * abs(ll_ref), (ll, ll_ref)
+    if grad:
+        _, scale = oracle.grad_scale(cat, p, variant)
+        check_grad(g, g_ref, scale)
+    return ll, g
+
+
+# ---- reference golden vectors ------------------------------------------------
+
+@pytest.mark.parametrize("case", golden("acceptance1.json"), ids=lambda c: f"n{c['n']}v{c['variant']}")
+def test_acceptance1_catalogs(eng, oracle, case):
+    """acceptance.cpp:50-84 (criterion 1) catalogs: engine vs the reference's
+    naive evaluator and its partitioned evaluator at G in {1,2,4,8}."""
+    cat = golden_catalog(case)
+    ll = eng.Evaluator(eng.Catalog(*cat)).eval(hp(eng, case["params"], case["variant"]))
+    ref = case["naive"]
+    assert abs(ll - ref) <= LL_TOL * abs(ref)
+    for v in case["ll"].values():
+        assert abs(ll - v) <= LL_TOL * abs(v)
+
+
+@pytest.mark.parametrize("case", golden("acceptance1.json")[:10], ids=lambda c: f"n{c['n']}v{c['variant']}")
+def test_acceptance1_gradient(eng, oracle, case):
+    run_vs_oracle(eng, oracle, golden_catalog(case), case["params"], case["variant"])
+
+
+@pytest.mark.parametrize("case", golden("engine_catalogs.json"), ids=lambda c: f"{c['kind']}{c['n']}v{c['variant']}")
+def test_engine_catalogs(eng, oracle, case):
+    """test_engine.cpp:127-141 / test_model.cpp:196-218 style catalogs incl.
+    tie-heavy times: whole-catalog LL and per-row event_contribution."""
+    cat = tuple(np.array(a) for a in case["catalog"])
+    ev = eng.Evaluator(eng.Catalog(*cat))
+    p = hp(eng, case["params"], case["variant"])
+    ll = ev.eval(p)
+    assert abs(ll - case["naive"]) <= LL_TOL * abs(case["naive"])
+    for g, v in case["ll"].items():
+        assert abs(ll - v) <= LL_TOL * abs(v)
+    for r, want in zip(case["rows"], case["event_contribution"]):
+        got = ev.eval_rows(p, r, r + 1)[0]
+        assert abs(got - want) <= 1e-12 * max(1.0, abs(want))
+    run_vs_oracle(eng, oracle, cat, case["params"], case["variant"])
+
+
+@pytest.mark.parametrize("case", golden("gradient_fd.json"), ids=lambda c: f"{c['kind']}v{c['variant']}")
+def test_gradient_vs_reference_fd(eng, oracle, case):
+    cat = eng.benchmark_catalog(case["n"], case["seed"]).arrays()
+    if case["kind"] == "ties":
+        cat = (np.round(cat[0] * 7) / 7,) + tuple(cat[1:])
+    _, g = eng.Evaluator(eng.Catalog(*cat)).eval(hp(eng, case["params"], case["variant"]), grad=True)
+    _, scale = oracle.grad_scale(cat, case["params"], case["variant"])
+    fd = np.array(case["grad_fd"])
+    check_grad(g, fd, scale, tol=1e-9)  # FD-limited (fd_err ~ 1e-11 of scale)
+    run_vs_oracle(eng, oracle, cat, case["params"], case["variant"])
+
+
+def test_kats(eng):
+    k = golden("kats.json")
+    unit = eng.HawkesParams()
+    solo = eng.Catalog([0.0], [0.0], [0.0])
+    ll, g = eng.Evaluator(solo).eval(unit, grad=True)
+    assert ll == pytest.approx(k["solo_clip"], rel=1e-12)  # test_engine.cpp:86-91
+    assert g[2] == 0.0 and g[3] == 0.0  # clipped row: no rate-term derivative
+    two = eng.Catalog(*k["two"]["catalog"])
+    assert eng.event_contribution(unit, two, 1) == pytest.approx(k["two"]["event_contribution_1"], rel=1e-12)
+    far = eng.Catalog(*k["far"]["catalog"])
+    ev = eng.Evaluator(far)
+    for n in range(4):  # the clip floor engages exactly (test_model.cpp:185-193)
+        got = ev.eval_rows(unit, n, n + 1)[0]
+        assert got == pytest.approx(k["far"]["event_contribution"][n], rel=1e-15)
+    assert ev.eval(unit) == pytest.approx(k["far"]["log_likelihood"], rel=1e-14)
+
+
+def test_workspace_semantics(eng):
+    """LikelihoodWorkspace script of test_engine.cpp:159-190 against the
+    reference workspace's own values."""
+    w = golden("workspace.json")
+    cat = eng.Catalog(*w["catalog"])
+    ws = eng.LikelihoodWorkspace(cat, eng.Variant.constant, 2)
+    for op, p, want in zip(w["ops"], w["params"], w["values"]):
+        p = hp(eng, p, 0)
+        if op == 0:
+            got = ws.evaluate_full(p)
+        elif op == 1:
+            got = ws.evaluate_proposal(p)
+        else:
+            ws.commit_proposal()
+            continue
+        assert abs(got - want) <= LL_TOL * abs(want)
+
+
+# ---- properties ------------------------------------------------------------------
+
+def test_determinism_bitwise(eng):
+    cat = eng.benchmark_catalog(6000, 47)
+    ev = eng.Evaluator(cat)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant.varying)
+    a = ev.eval(p, grad=True)
+    b = ev.eval(p, grad=True)
+    c = eng.Evaluator(cat).eval(p, grad=True)
+    assert a[0] == b[0] == c[0]
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[1], c[1])
+
+
+def test_variant_collapse_bitwise(eng):
+    """acceptance.cpp:325-344 (criterion 8): unit densities make the varying
+    variant bitwise equal to the constant one."""
+    rng = np.random.default_rng(808)
+    for c in range(6):
+        t, x, y, _ = eng.benchmark_catalog(int(rng.integers(10, 2000)), 7000 + c).arrays()
+        cat = eng.Catalog(t, x, y, np.ones_like(t))
+        ev = eng.Evaluator(cat)
+        base = dict(mu0=rng.uniform(0.1, 2), tau_t=rng.uniform(0.5, 20), xi0=rng.uniform(0.05, 0.9),
+                    sigma_x=rng.uniform(0.02, 0.5), sigma_t=rng.uniform(0.2, 10), area=100.0)
+        a = ev.eval(eng.HawkesParams(**base, variant=eng.Variant.constant), grad=True)
+        b = ev.eval(eng.HawkesParams(**base, variant=eng.Variant.varying), grad=True)
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])
+
+
+def test_translation_invariance(eng, oracle):
+    # test_model.cpp:249-262
+    t, x, y, d = eng.benchmark_catalog(900, 37).arrays()
+    p = eng.HawkesParams(mu0=0.7, tau_t=3.0, xi0=0.4, sigma_x=0.3, sigma_t=1.5, area=80.0)
+    a = eng.Evaluator(eng.Catalog(t, x, y, d)).eval_rows(p, 0, 900)
+    b = eng.Evaluator(eng.Catalog(t, x + 13.75, y - 4.5, d)).eval_rows(p, 0, 900)
+    np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-12)
+
+
+def test_row_sum_equals_total(eng):
+    # test_engine.cpp:76-84 (single slice == sum of event contributions)
+    cat = eng.benchmark_catalog(1200, 41)
+    p = eng.HawkesParams(**BENCH)
+    ev = eng.Evaluator(cat)
+    ell, g = ev.eval_rows(p, 0, 1200, grad=True)
+    ll, gt = ev.eval(p, grad=True)
+    assert math.fsum(ell) == pytest.approx(ll, rel=1e-13)
+    np.testing.assert_allclose(g.sum(axis=0), gt, rtol=1e-11, atol=1e-9)
+
+
+def test_shards_sum_to_total(eng):
+    """Row shards (the one-process-per-GPU path, here two contexts on one
+    device) reduce, in rank order, to the single-context result."""
+    cat = eng.benchmark_catalog(20000, 3)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant.varying)
+    full = eng.Evaluator(cat).eval(p, grad=True)
+    for g in (2, 3, 8):
+        b = eng.plan_shards(cat.t, g)
+        parts = [eng.Evaluator(cat, shard=(int(b[i]), int(b[i + 1]))).eval(p, grad=True) for i in range(g)]
+        ll = sum(x[0] for x in parts)
+        gr = np.sum([x[1] for x in parts], axis=0)
+        assert ll == pytest.approx(full[0], rel=1e-12)
+        np.testing.assert_allclose(gr, full[1], rtol=1e-10, atol=1e-8)
+
+
+def test_set_locations(eng, oracle):
+    cat = eng.benchmark_catalog(3000, 11)
+    ev = eng.Evaluator(cat)
+    rng = np.random.default_rng(3)
+    lon, lat = rng.uniform(-5, 5, 3000), rng.uniform(-5, 5, 3000)
+    ev.set_locations(lon, lat)
+    p = dict(BENCH)
+    ll, g = ev.eval(hp(eng, p, 1), grad=True)
+    ref, gref = oracle.ll_grad((cat.t, lon, lat, cat.density), p, 1)
+    assert abs(ll - ref) <= LL_TOL * abs(ref)
+    _, scale = oracle.grad_scale((cat.t, lon, lat, cat.density), p, 1)
+    check_grad(g, gref, scale)
+
+
+def test_errors(eng):
+    cat = eng.benchmark_catalog(100, 1)
+    ev = eng.Evaluator(cat)
+    with pytest.raises(ValueError, match="sigma_t must be positive"):
+        ev.eval(eng.HawkesParams(sigma_t=-1.0))
+    with pytest.raises(IndexError):
+        ev.eval_rows(eng.HawkesParams(), 50, 101)
+    with pytest.raises(IndexError):
+        eng.event_contribution(eng.HawkesParams(), cat, 100)
+    with pytest.raises(ValueError, match="partition does not cover"):
+        eng.log_likelihood(cat, eng.HawkesParams(), eng.Partition.make(99, 2))
+    with pytest.raises(ValueError, match="double precision only"):
+        eng.log_likelihood(cat, eng.HawkesParams(), eng.Partition.make(100, 2), eng.Precision.single)
+
+
+def test_adversarial_finite(eng, oracle):
+    """acceptance.cpp:86-113 / test_engine.cpp:143-157 catalogs (coincident
+    events, widely separated events): finite and equal to the oracle."""
+    n = 3000
+    coincident = eng.Catalog(np.arange(n) * 0.01, np.full(n, 0.5), np.full(n, 0.5))
+    p = dict(mu0=1.0, tau_t=1.0, xi0=1.0, sigma_x=1e-3, sigma_t=1.0, area=1.0)
+    run_vs_oracle(eng, oracle, coincident.arrays(), p, 0)
+    i = np.arange(n)
+    sep = eng.Catalog(i * 10.0, np.where(i % 2, 1.0, -1.0) * 1e4, np.where(i % 3, 1.0, -1.0) * 1e4)
+    run_vs_oracle(eng, oracle, sep.arrays(), p, 0)
+    same = eng.Catalog(np.zeros(2000), np.zeros(2000), np.zeros(2000))  # all tied: every row clipped
+    ll = eng.Evaluator(same).eval(eng.HawkesParams())
+    assert ll == pytest.approx(oracle.ll_grad(same.arrays(), [1.0] * 6, 0)[0], rel=1e-12)
+
+
+def test_random_params_sweep(eng, oracle):
+    """Random catalogs and parameters over the reference test ranges,
+    including sizes around the 256-row/column tile edges."""
+    rng = np.random.default_rng(2024)
+    for c, n in enumerate([1, 2, 3, 31, 255, 256, 257, 511, 513, 1000, 2049, 4100]):
+        cat = float_round(eng.benchmark_catalog(n, 300 + c).arrays())
+        p = dict(mu0=rng.uniform(0.1, 2), tau_t=rng.uniform(0.5, 20), xi0=rng.uniform(0.05, 0.9),
+                 sigma_x=rng.uniform(0.02, 0.5), sigma_t=rng.uniform(0.2, 10), area=100.0)
+        for v in (0, 1):
+            run_vs_oracle(eng, oracle, cat, p, v, grad=n > 1)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_bench_config_100k_sampled_rows(eng, oracle, variant):
+    """N=1e5 benchmark catalog: 512 sampled rows (value + gradient) against
+    the long-double oracle, per row 1e-12."""
+    cat = eng.benchmark_catalog(100000, 42)
+    ev = eng.Evaluator(cat)
+    p = hp(eng, BENCH, variant)
+    rows = np.linspace(0, 99999, 512).astype(np.int64)
+    res = [ev.eval_rows(p, int(r), int(r) + 1, grad=True) for r in rows]
+    got = np.array([e[0][0] for e in res])
+    gg = np.array([e[1][0] for e in res])
+    want, gw = oracle.rows_ld(cat.arrays(), BENCH, variant, rows.astype(np.uint64))
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(gg, gw, rtol=1e-10, atol=1e-10 * np.abs(gw).max())
+
+
+def test_bench_config_100k_reference_full(eng, reference):
+    """N=1e5 full log-likelihood against the reference's own partitioned CPU
+    evaluator (oracle/_ref) on all host threads."""
+    import os
+    cat = eng.benchmark_catalog(100000, 42)
+    if (os.cpu_count() or 1) < 32:
+        pytest.skip("full 1e5 reference run needs >= 32 host threads to stay short")
+    p = eng.HawkesParams(**BENCH)
+    ll = eng.Evaluator(cat).eval(p)
+    ref = reference.log_likelihood(cat.arrays(), BENCH, 0, workers=os.cpu_count())
+    assert abs(ll - ref) <= LL_TOL * abs(ref)
+
+
+def test_1m_sampled_rows(eng, oracle):
+    """N=1e6 (BASELINE config): 1024 evenly spaced rows vs the oracle (SURVEY.md
+    8c), plus the whole-catalog LL+grad is finite and deterministic."""
+    cat = eng.benchmark_catalog(1000000, 42)
+    ev = eng.Evaluator(cat)
+    p = hp(eng, BENCH, 0)
+    rows = np.linspace(0, 999999, 1024).astype(np.int64)
+    got = np.array([ev.eval_rows(p, int(r), int(r) + 1)[0] for r in rows])
+    want = oracle.rows_ld(cat.arrays(), BENCH, 0, rows.astype(np.uint64), grad=False)
+    np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+    # a contiguous window through the same path as the full evaluation
+    win, gwin = ev.eval_rows(p, 500000, 500256, grad=True)
+    wr = np.arange(500000, 500256, dtype=np.uint64)
+    want_w, gw = oracle.rows_ld(cat.arrays(), BENCH, 0, wr)
+    np.testing.assert_allclose(win, want_w, rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(gwin, gw, rtol=1e-10, atol=1e-10 * np.abs(gw).max())
+    a = ev.eval(p, grad=True)
+    b = ev.eval(p, grad=True)
+    assert np.isfinite(a[0]) and a[0] == b[0] and np.array_equal(a[1], b[1])

@@ -1,0 +1,197 @@
+"""CPU tests: the oracle pinned to the reference's golden vectors, and the
+product's host logic (catalog generator, partition, shard planner) pinned to
+the same vectors.  No GPU needed."""
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_catalog
+
+PKEYS = ("mu0", "tau_t", "xi0", "sigma_x", "sigma_t", "area")
+
+
+def digest(arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a, dtype="<f8").tobytes())
+    return h.hexdigest()
+
+
+# ---- product host logic vs reference vectors -------------------------------
+
+@pytest.mark.parametrize("case", golden("benchmark_catalog.json"), ids=lambda c: f"n{c['n']}s{c['seed']}")
+def test_benchmark_catalog_bit_identical(case):
+    from paper_2407_11349_b200 import benchmark_catalog
+    cat = benchmark_catalog(case["n"], case["seed"]).arrays()
+    assert digest(cat) == case["sha256"]
+    for i, row in enumerate(case["head"]):
+        assert [float(a[i]) for a in cat] == row
+
+
+@pytest.mark.parametrize("case", golden("partition.json"), ids=lambda c: f"{c['n']}_{c['g']}")
+def test_partition_make_matches_reference(case):
+    from paper_2407_11349_b200 import Partition
+    p = Partition.make(case["n"], case["g"])
+    b = case["bounds"]
+    assert p.ranges == list(zip(b[:-1], b[1:]))
+
+
+def test_partition_errors():
+    from paper_2407_11349_b200 import Partition
+    with pytest.raises(ValueError, match="worker count must be positive"):
+        Partition.make(5, 0)
+    with pytest.raises(ValueError, match="more workers than terms"):
+        Partition.make(5, 6)
+
+
+def test_partition_invariants_random():
+    # test_engine.cpp:19-37 ("partition invariants hold for random shapes")
+    from paper_2407_11349_b200 import Partition
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        n = int(rng.integers(1, 5001))
+        g = int(rng.integers(1, n + 1))
+        r = Partition.make(n, g).ranges
+        assert len(r) == g and r[0][0] == 0 and r[-1][1] == n
+        lens = [e - b for b, e in r]
+        assert min(lens) > 0 and max(lens) - min(lens) <= 1
+        assert all(r[i][1] == r[i + 1][0] for i in range(g - 1))
+
+
+def test_plan_shards_balanced():
+    from paper_2407_11349_b200 import benchmark_catalog, plan_shards
+    t = benchmark_catalog(200000, 42).t
+    lb = np.searchsorted(t, t, side="left")
+    for g in (1, 2, 4, 8):
+        b = plan_shards(t, g)
+        assert b[0] == 0 and b[-1] == len(t) and np.all(np.diff(b) > 0)
+        cost = 13.0 * (len(t) - 1) + 17.0 * lb
+        w = np.array([cost[b[i]:b[i + 1]].sum() for i in range(g)])
+        assert w.max() / w.mean() < 1.001
+    # the uniform partition is ~26% imbalanced at G=8
+    u = np.linspace(0, len(t), 9).astype(int)
+    wu = np.array([cost[u[i]:u[i + 1]].sum() for i in range(8)])
+    assert wu.max() / wu.mean() > 1.2
+
+
+def test_plan_shards_ties_and_errors():
+    from paper_2407_11349_b200 import plan_shards
+    t = np.repeat(np.arange(10.0), 5)
+    b = plan_shards(t, 4)
+    assert b[0] == 0 and b[-1] == 50 and np.all(np.diff(b) > 0)
+    with pytest.raises(ValueError):
+        plan_shards(t, 0)
+    with pytest.raises(ValueError, match="not sorted"):
+        plan_shards(t[::-1].copy(), 2)
+
+
+# ---- catalog / params validation (types.hpp:43-57, 92-103) -----------------
+
+def test_catalog_validation_messages():
+    from paper_2407_11349_b200 import Catalog
+    with pytest.raises(ValueError, match="need at least one event"):
+        Catalog([], [], [])
+    with pytest.raises(ValueError, match="event 0 has invalid time"):
+        Catalog([-1.0], [0.0], [0.0])
+    with pytest.raises(ValueError, match="event 0 has nonpositive density"):
+        Catalog([0.0], [0.0], [0.0], [-2.0])
+    with pytest.raises(ValueError, match="event 0 has non-finite location"):
+        Catalog([0.0], [math.nan], [0.0])
+    with pytest.raises(ValueError, match="times not sorted at index 1"):
+        Catalog([2.0, 1.0, 3.0], [0, 0.5, -1], [0, 0.5, 1])
+    c = Catalog.sorted([2.0, 1.0, 3.0], [0, 0.5, -1], [0, 0.5, 1])
+    assert list(c.t) == [1.0, 2.0, 3.0] and list(c.lon) == [0.5, 0, -1]
+
+
+def test_params_validation():
+    from paper_2407_11349_b200 import HawkesParams
+    HawkesParams().validate()
+    for k in PKEYS:
+        with pytest.raises(ValueError, match=f"HawkesParams: {k} must be positive and finite"):
+            HawkesParams(**{k: 0.0}).validate()
+        with pytest.raises(ValueError, match=k):
+            HawkesParams(**{k: math.inf}).validate()
+
+
+# ---- oracle vs reference golden vectors ------------------------------------
+
+def test_oracle_kats(oracle):
+    k = golden("kats.json")
+    for z, v in k["gaussian_pdf"].items():
+        assert oracle.L.orc_gaussian_pdf(float(z)) == v
+    for z, v in k["gaussian_cdf"].items():
+        assert oracle.L.orc_gaussian_cdf(float(z)) == v
+    unit = [1.0] * 6
+    assert oracle.pair_rate(unit, 0, [0, 0, 0, 1], [1, 0, 0, 1]) == k["pair_rate_forward"]
+    assert oracle.pair_rate(unit, 0, [0, 0, 0, 1], [0, 0, 0, 1]) == k["pair_rate_same"] == 0.0
+    assert oracle.pair_rate(unit, 0, [1, 0, 0, 1], [0, 0, 0, 1]) == k["pair_rate_reverse"]
+    assert oracle.integral_term(unit, 0.0, 1.0) == k["integral_unit_0_1"]
+    assert oracle.integral_term(unit, 0.0, 0.0) == k["integral_unit_0_0"] == 0.0
+    # test_model.cpp:104-113 / :139-141 published constants
+    assert k["pair_rate_forward"] == pytest.approx(0.3005205560434625, rel=1e-12)
+    assert k["pair_rate_reverse"] == pytest.approx(0.24197072451914337, rel=1e-12)
+    assert k["integral_unit_0_1"] == pytest.approx(0.9734653048971006, rel=1e-12)
+    assert k["solo_clip"] == pytest.approx(-92.10340371976183, rel=1e-12)
+    assert oracle.log_likelihood(([0.0], [0.0], [0.0], [1.0]), unit, 0) == k["solo_clip"]
+
+
+@pytest.mark.parametrize("case", golden("acceptance1.json")[:12], ids=lambda c: f"n{c['n']}v{c['variant']}")
+def test_oracle_lanes_match_reference_bitwise(oracle, case):
+    cat = golden_catalog(case)
+    assert digest(cat) == case["sha256"]
+    for g, v in case["ll"].items():
+        assert oracle.log_likelihood(cat, case["params"], case["variant"], int(g)) == pytest.approx(v, rel=1e-13)
+    assert oracle.naive_log_likelihood(cat, case["params"], case["variant"]) == pytest.approx(case["naive"], rel=1e-14)
+
+
+@pytest.mark.parametrize("case", golden("engine_catalogs.json"), ids=lambda c: f"{c['kind']}{c['n']}v{c['variant']}")
+def test_oracle_engine_catalogs(oracle, case):
+    cat = tuple(np.array(a) for a in case["catalog"])
+    p, v = case["params"], case["variant"]
+    assert oracle.naive_log_likelihood(cat, p, v) == pytest.approx(case["naive"], rel=1e-14)
+    for g, val in case["ll"].items():
+        assert oracle.log_likelihood(cat, p, v, int(g)) == pytest.approx(val, rel=1e-13)
+    ld, _ = oracle.ll_grad(cat, p, v)
+    assert ld == pytest.approx(case["naive"], rel=1e-12)
+    ell = oracle.rows_ld(cat, p, v, case["rows"], grad=False)
+    np.testing.assert_allclose(ell, case["event_contribution"], rtol=1e-12, atol=1e-12)
+
+
+def test_oracle_far_catalog_clip(oracle):
+    k = golden("kats.json")["far"]
+    cat = tuple(np.array(a) for a in k["catalog"])
+    ell = oracle.rows_ld(cat, k["params"], 0, range(4), grad=False)
+    for n in range(4):
+        assert ell[n] == pytest.approx(k["event_contribution"][n], rel=1e-15)
+        assert k["event_contribution"][n] == math.log(1e-40) - k["integral"][n]
+
+
+@pytest.mark.parametrize("case", golden("gradient_fd.json"), ids=lambda c: f"{c['kind']}v{c['variant']}")
+def test_oracle_gradient_pinned_by_reference_fd(oracle, case):
+    """The gradient restatement vs Richardson central differences of the
+    reference's log_likelihood (conditioning-aware scale)."""
+    from paper_2407_11349_b200 import benchmark_catalog
+    cat = benchmark_catalog(case["n"], case["seed"]).arrays()
+    if case["kind"] == "ties":
+        cat = (np.round(cat[0] * 7) / 7,) + tuple(cat[1:])
+    _, g = oracle.ll_grad(cat, case["params"], case["variant"])
+    _, scale = oracle.grad_scale(cat, case["params"], case["variant"])
+    fd = np.array(case["grad_fd"])
+    err = np.abs(g - fd) / np.maximum(np.abs(fd), scale)
+    assert np.all(err < 1e-9), err
+
+
+def test_oracle_long_double_vs_reference(oracle):
+    case = golden("acceptance1.json")[5]
+    cat = golden_catalog(case)
+    ld, _ = oracle.ll_grad(cat, case["params"], case["variant"])
+    assert ld == pytest.approx(case["naive"], rel=1e-13)
+
+
+def test_reference_lib_matches_goldens(reference):
+    """Where oracle/_ref exists, it still reproduces the committed vectors."""
+    case = golden("acceptance1.json")[1]
+    cat = golden_catalog(case)
+    assert reference.log_likelihood(cat, case["params"], case["variant"], 2) == case["ll"]["2"]
