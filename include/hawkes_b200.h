@@ -113,6 +113,13 @@ void* hk_stream(hk_ctx* ctx, int dev);
 int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* ell_rows,
                  double* grad_rows);
 
+/* Evaluation options (all default on).
+ *   HK_OPT_BG_EXPANSION: evaluate the background sum of qualifying tile
+ *     pairs by the exact block expansion instead of
+ *     per pair; 0 forces the direct per-pair path everywhere. */
+#define HK_OPT_BG_EXPANSION 1
+int hk_set_option(hk_ctx* ctx, int option, int value);
+
 /* Rows [begin, end) this context evaluates, and its device count. */
 int hk_rows(const hk_ctx* ctx, size_t* begin, size_t* end, int* n_devices);
 

@@ -25,6 +25,7 @@ if not LIB_PATH.exists():
 lib = C.CDLL(str(LIB_PATH))
 
 HK_OK, HK_INVALID_ARGUMENT, HK_OUT_OF_RANGE, HK_RUNTIME_ERROR, HK_NOT_IMPLEMENTED = range(5)
+HK_OPT_BG_EXPANSION = 1
 
 
 class hk_params(C.Structure):
@@ -51,6 +52,7 @@ SIGNATURES = [
     ("hk_result_device", C.c_void_p, [_ctx]),
     ("hk_stream", C.c_void_p, [_ctx, C.c_int]),
     ("hk_eval_rows", C.c_int, [_ctx, _pp, _sz, _sz, _dp, C.c_void_p]),
+    ("hk_set_option", C.c_int, [_ctx, C.c_int, C.c_int]),
     ("hk_rows", C.c_int, [_ctx, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int)]),
     ("hk_set_profiling", C.c_int, [_ctx, C.c_int]),
     ("hk_profile", C.c_int, [_ctx, C.POINTER(C.c_double), C.POINTER(C.c_long), C.POINTER(C.c_long)]),

@@ -98,6 +98,7 @@ struct hk_ctx {
   double d2_max = 0.0, q_max = 1.0;
   std::vector<DeviceState> devs;
   bool profiling = false;
+  int bg_expansion = 1;
   double prof_ms = 0.0;
   long prof_pair = 0, prof_total = 0;
 
@@ -190,7 +191,9 @@ struct hk_ctx {
     if (!p) throw std::invalid_argument("hk_eval: null params");
     const hk::ParamsIn in{p->mu0, p->tau_t, p->xi0, p->sigma_x, p->sigma_t, p->area, p->variant};
     hk::validate_params(in);
-    return hk::make_coef(in, t[0], t[n - 1], d2_max, q_max);
+    hk::EvalCoef c = hk::make_coef(in, t[0], t[n - 1], d2_max, q_max);
+    c.bg_expansion = bg_expansion;
+    return c;
   }
 
   // Enqueues prep + pair + finish + reduce for device s.
@@ -421,6 +424,14 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
       throw;
     }
     cleanup();
+  });
+}
+
+int hk_set_option(hk_ctx* ctx, int option, int value) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("hk_set_option: null context");
+    if (option == HK_OPT_BG_EXPANSION) ctx->bg_expansion = value != 0;
+    else throw std::invalid_argument("hk_set_option: unknown option " + std::to_string(option));
   });
 }
 

@@ -211,10 +211,13 @@ EvalCoef make_coef(const ParamsIn& p, double t_min, double t_max, double d2_max,
   c.a = p.mu0 * inv_area * c.tau_prec * kInvSqrt2Pi;         // model.hpp:329-331
   c.c = p.xi0 * c.omega * c.sx_prec * c.sx_prec * kInv2Pi;   // model.hpp:333-336
   c.half_s2 = 0.5 * c.sx_prec * c.sx_prec;                   // model.hpp:277
-  c.Kb = -0.5 * c.tau_prec * c.tau_prec * kLog2e16;
-  c.Kq0 = -c.half_s2 * kLog2e16;
-  c.Kw = -c.omega * kLog2e16;
+  c.Kb = -0.5 * c.tau_prec * c.tau_prec * kLog2eT;
+  c.Kq0 = -c.half_s2 * kLog2eT;
+  c.Kw = -c.omega * kLog2eT;
   c.t_end = t_max;
+  c.u_scale = c.tau_prec * 0.7071067811865476;
+  c.two_tau2 = 2.0 * p.tau_t * p.tau_t;
+  c.bg_expansion = 1;
   c.varying = p.variant;
   const double span = t_max - t_min;
   const double qm = p.variant ? q_max : 1.0;

@@ -44,7 +44,27 @@ namespace hk {
 
 namespace {
 
-enum TileType { kSkip = 0, kTileBT = 1, kTileB = 2, kTileT = 3, kTileM = 4 };
+enum TileType { kSkip = 0, kTileBT = 1, kTileB = 2, kTileT = 3, kTileM = 4, kTileBTx = 5, kTileBx = 6 };
+
+// Background block expansion (tiles BTx / Bx).  With u = t/(tau sqrt2),
+// row offsets alpha_i = u_i - c_I, column offsets beta_j = u_j - c_J and
+// D = c_I - c_J (block and tile centres), the background kernel factors
+// EXACTLY as
+//   exp(-(u_i-u_j)^2) = exp(-(D+alpha_i)^2) * exp(2 D beta_j - beta_j^2)
+//                       * exp(2 alpha_i beta_j),
+// and the last factor is expanded as sum_{n<=kXP} (2 alpha beta)^n / n!.
+// A tile pair qualifies only when eps = max|2 alpha beta| <= kEpsMax, where
+// the truncated remainder eps^(kXP+1)/(kXP+1)! e^(2 eps) < 4e-21, far below
+// one ulp of every term; otherwise the direct per-pair path runs.  Then
+//   B_i  += R_i * sum_n (2 alpha_i)^n/n! M_n,         M_n = sum_j C_j beta_j^n
+//   B2_i += 2 tau^2 R_i * sum_j (gamma_i - beta_j)^2 C_j X_ij,  gamma_i = D + alpha_i
+// i.e. 256 column exps + 9 moment sums per tile and ~25 FP64 per row per
+// tile, instead of 13 FP64 per pair.  At N=1e6 blocks span ~0.026 weeks and
+// eps ~ 7e-6.
+constexpr int kXP = 6;
+constexpr int kNM = kXP + 3;  // moments M_0 .. M_{kXP+2} (B2 needs two more)
+constexpr double kEpsMax = 4.0e-3;
+constexpr double kDBetaMax = 4.0;  // |2 D beta| bound: column factors stay below e^4
 
 // Shared-memory slots of one staged tile.
 enum Slot { sT = 0, sX, sY, sW, sV, sZ, sK, sAux, kSlots };
@@ -103,6 +123,15 @@ struct BlockInfo {
   double t_first, t_last;
 };
 
+__device__ __forceinline__ bool expansion_ok(const BlockInfo& bi, double t0, double t1,
+                                             const EvalCoef& c) {
+  if (!c.bg_expansion) return false;
+  const double hI = 0.5 * c.u_scale * (bi.t_last - bi.t_first);
+  const double hJ = 0.5 * c.u_scale * (t1 - t0);
+  const double D = c.u_scale * (0.5 * (bi.t_first + bi.t_last) - 0.5 * (t0 + t1));
+  return 2.0 * hI * hJ <= kEpsMax && 2.0 * fabs(D) * hJ <= kDBetaMax;
+}
+
 __device__ __forceinline__ int tile_type(int J, const BlockInfo& bi, const PairParams& P) {
   const int j0 = J * kBJ, j1 = j0 + kBJ;
   const double* __restrict__ t = P.d.t;
@@ -111,11 +140,14 @@ __device__ __forceinline__ int tile_type(int J, const BlockInfo& bi, const PairP
     const double td = bi.t_first - t[j1 - 1];
     const bool bg_far = td * td * (-P.c.Kb) > kFlushArg;
     const bool tr_far = td * (-P.c.Kw) > kFlushArg;
-    return bg_far ? (tr_far ? kSkip : kTileT) : (tr_far ? kTileB : kTileBT);
+    if (bg_far) return tr_far ? kSkip : kTileT;
+    const bool x = expansion_ok(bi, t[j0], t[j1 - 1], P.c);
+    return tr_far ? (x ? kTileBx : kTileB) : (x ? kTileBTx : kTileBT);
   }
   if (j0 >= bi.ubmax && j1 <= P.d.n) {
     const double td = t[j0] - bi.t_last;
-    return td * td * (-P.c.Kb) > kFlushArg ? kSkip : kTileB;
+    if (td * td * (-P.c.Kb) > kFlushArg) return kSkip;
+    return expansion_ok(bi, t[j0], t[j1 - 1], P.c) ? kTileBx : kTileB;
   }
   return kTileM;
 }
@@ -126,12 +158,12 @@ __device__ __forceinline__ void issue_tile(int type, int J, double* buf, uint64_
   const int j0 = J * kBJ;
   constexpr unsigned kBytes = kBJ * sizeof(double);
   unsigned mask = 0;
-  if (type == kTileB) {
+  if (type == kTileB || type == kTileBx) {
     mask = 1u << sT;
   } else if (type == kTileM) {
     mask = (1u << sT) | (1u << sX) | (1u << sY);
     if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = q
-  } else {  // BT or T
+  } else {  // BT, BTx or T
     mask = (1u << sT) | (1u << sX) | (1u << sY) | (1u << sW);
     if (kGrad) mask |= (1u << sV) | (1u << sZ);
     if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = thr
@@ -232,6 +264,65 @@ __device__ __forceinline__ void tile_fast(RowState& R, const double* __restrict_
   }
 }
 
+// Background of a whole BTx/Bx tile by the block expansion (see kXP).
+template <bool kGrad>
+__device__ __forceinline__ void bg_expansion(RowState& R, const double* __restrict__ st,
+                                             const BlockInfo& bi, const EvalCoef& c,
+                                             double (*s_red)[kNM]) {
+  const double s = c.u_scale;
+  const double cI = 0.5 * (bi.t_first + bi.t_last);
+  const double cJ = 0.5 * (st[0] + st[kBJ - 1]);
+  const double D = s * (cI - cJ);
+  double m[kNM];
+#pragma unroll
+  for (int n = 0; n < kNM; ++n) m[n] = 0.0;
+  for (int jj = threadIdx.x; jj < kBJ; jj += kThreads) {
+    const double beta = s * (st[jj] - cJ);
+    double p = exp(fma(2.0 * D, beta, -beta * beta));  // column factor C_j
+#pragma unroll
+    for (int n = 0; n < kNM; ++n) {
+      m[n] += p;
+      p *= beta;
+    }
+  }
+  // fixed-order reduction over the CTA: warp butterfly, then warps in order
+#pragma unroll
+  for (int n = 0; n < kNM; ++n)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m[n] += __shfl_xor_sync(0xffffffffu, m[n], off);
+  const int warp = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int n = 0; n < kNM; ++n) s_red[warp][n] = m[n];
+  __syncthreads();
+#pragma unroll
+  for (int n = 0; n < kNM; ++n) {
+    double a = s_red[0][n];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) a += s_red[w][n];
+    m[n] = a;
+  }
+#pragma unroll
+  for (int r = 0; r < kRowsPerThread; ++r) {
+    const double alpha = s * (R.t[r] - cI);
+    const double gamma = D + alpha;
+    const double x = 2.0 * alpha;
+    double S0 = m[kXP], S1 = m[kXP + 1], S2 = m[kXP + 2];
+#pragma unroll
+    for (int n = kXP; n >= 1; --n) {
+      const double xn = x * (1.0 / n);
+      S0 = fma(xn, S0, m[n - 1]);
+      if (kGrad) {
+        S1 = fma(xn, S1, m[n]);
+        S2 = fma(xn, S2, m[n + 1]);
+      }
+    }
+    const double Rf = exp(-gamma * gamma);  // row factor R_i
+    R.B[r] = fma(Rf, S0, R.B[r]);
+    if (kGrad) R.B2[r] = fma(Rf * c.two_tau2, fma(gamma, fma(gamma, S0, -2.0 * S1), S2), R.B2[r]);
+  }
+}
+
 // M tiles: the reference's exact value guards, per pair.
 template <bool kVarying, bool kGrad, int kMode>
 __device__ __forceinline__ void tile_masked(RowState& R, int j0, int n,
@@ -276,6 +367,7 @@ template <bool kVarying, bool kGrad, int kMode>
 __global__ void __launch_bounds__(kThreads, HK_MIN_BLOCKS) pair_kernel(const PairParams P) {
   __shared__ __align__(128) double s_buf[2][kSlots * kBJ];
   __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ double s_red[kThreads / 32][kNM];
 
   const int tid = threadIdx.x;
   const Item it = P.items[blockIdx.x];
@@ -338,6 +430,13 @@ __global__ void __launch_bounds__(kThreads, HK_MIN_BLOCKS) pair_kernel(const Pai
       case kTileT:
         tile_fast<kVarying, kGrad, kMode, false, true>(R, buf, P.c);
         break;
+      case kTileBTx:
+        bg_expansion<kGrad>(R, buf + sT * kBJ, bi, P.c, s_red);
+        tile_fast<kVarying, kGrad, kMode, false, true>(R, buf, P.c);
+        break;
+      case kTileBx:
+        bg_expansion<kGrad>(R, buf + sT * kBJ, bi, P.c, s_red);
+        break;
       default:
         tile_masked<kVarying, kGrad, kMode>(R, cur * kBJ, P.d.n, buf, P.c);
         break;
@@ -369,7 +468,7 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
   if (j >= d.npad) return;
   if (j < d.n) {
     const double q = c.varying ? d.q[j] : 1.0;
-    const double K = -(c.half_s2 * q) * kLog2e16;
+    const double K = -(c.half_s2 * q) * kLog2eT;
     const int jr = min(d.n, (j / kBJ + 1) * kBJ) - 1;
     const double dtr = d.t[jr] - d.t[j];
     const double w = q * exp(-c.omega * dtr);

@@ -27,6 +27,9 @@ struct EvalCoef {
   double Kq0;     // -half_s2 * 16/ln2           (trigger exponent per d^2, q = 1)
   double Kw;      // -omega * 16/ln2             (trigger exponent per td)
   double t_end;   // t[N-1]
+  double u_scale; // 1 / (tau sqrt 2): background kernel = exp(-(u_i - u_j)^2)
+  double two_tau2;// 2 tau^2
+  int bg_expansion;  // 1: background by the exact block expansion where it qualifies
   int varying;
   int mode;       // ExpMode: kExact / kFlush / kChecked from the argument bound
 };

@@ -226,6 +226,11 @@ class Evaluator:
                                g.ctypes.data_as(C.c_void_p) if grad else None))
         return (ell, g) if grad else ell
 
+    def set_bg_expansion(self, on: bool) -> None:
+        """Exact block expansion of the background sum (default on); off
+        forces the direct per-pair path."""
+        check(lib.hk_set_option(self._h, _lib.HK_OPT_BG_EXPANSION, int(on)))
+
     def set_profiling(self, on: bool) -> None:
         check(lib.hk_set_profiling(self._h, int(on)))
 
