@@ -33,22 +33,32 @@
 
 namespace hk {
 
-// Kernel shape (overridable at build time for tuning experiments).
+// Kernel shape (overridable at build time for tuning experiments).  Rows
+// per thread differ by variant (measured, tools/tune_shapes.sh): the
+// constant kernel amortises each staged column over 4 rows; the varying
+// kernel keeps 2 so its per-row-slot skip votes stay cheap.
 #ifndef HK_THREADS
 #define HK_THREADS 128
 #endif
-#ifndef HK_ROWS_PER_THREAD
-#define HK_ROWS_PER_THREAD 2
+#ifndef HK_ROWS_CONST
+#define HK_ROWS_CONST 4
+#endif
+#ifndef HK_ROWS_VAR
+#define HK_ROWS_VAR 2
 #endif
 #ifndef HK_UNROLL
 #define HK_UNROLL 2
 #endif
-#ifndef HK_MIN_BLOCKS
-#define HK_MIN_BLOCKS 4
-#endif
-constexpr int kThreads = HK_THREADS;             // threads per CTA
-constexpr int kRowsPerThread = HK_ROWS_PER_THREAD;
-constexpr int kBI = kThreads * kRowsPerThread;   // rows per work item (one CTA)
+constexpr int kThreads = HK_THREADS;  // threads per CTA
+__host__ __device__ constexpr int rows_per_thread(bool varying) {
+  return varying ? HK_ROWS_VAR : HK_ROWS_CONST;
+}
+// rows per work item (one CTA)
+__host__ __device__ constexpr int rows_per_item(bool varying) {
+  return kThreads * rows_per_thread(varying);
+}
+// resident CTAs per SM the register budget is sized for (64K regs)
+__host__ __device__ constexpr int min_blocks(int rows) { return rows >= 4 ? 2 : (rows == 3 ? 2 : 4); }
 constexpr int kBJ = 256;                         // columns per shared-memory tile
 constexpr int kUnroll = HK_UNROLL;               // column-loop unroll of the fast tiles
 
@@ -153,11 +163,30 @@ __device__ __forceinline__ void load_exp2_table() {
   if (threadIdx.x < kTab) s_exp2_tab[threadIdx.x] = kExp2Tab[threadIdx.x];
 }
 
+// Polynomial coefficients in the constant bank: DFMA reads them as c[][]
+// operands instead of rematerialising 64-bit immediates into registers.
+__device__ __constant__ static double c_poly[kPolyTerms] = HK_POLY;  // non-const: not folded
+
+// Table entry k & (kTab-1): one mask + one multiply-add for the address.
+__device__ __forceinline__ double exp2_table(int k) {
+  unsigned addr;
+  asm("{\n"
+      ".reg .u32 i;\n"
+      "and.b32 i, %1, %2;\n"
+      "mad.lo.u32 %0, i, 8, %3;\n"
+      "}\n"
+      : "=r"(addr)
+      : "r"(k), "n"(kTab - 1), "r"(static_cast<unsigned>(__cvta_generic_to_shared(s_exp2_tab))));
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 // Completes 2^((k + r)/kTab) given t = MAGIC + k and the reduced r.
 template <int kMode>
 __device__ __forceinline__ double exp2_16_finish(double t, double r) {
   const int k = __double2loint(t);
-  const double T = s_exp2_tab[k & (kTab - 1)];
+  const double T = exp2_table(k);
   int hi = __double2hiint(T) + (k << (20 - kTabBits));
   int lo = __double2loint(T);
   if (kMode != kExact) {
@@ -169,9 +198,9 @@ __device__ __forceinline__ double exp2_16_finish(double t, double r) {
     hi = ok ? hi : 0;
     lo = ok ? lo : 0;
   }
-  double p = poly_coef(kPolyTerms - 1);
+  double p = c_poly[kPolyTerms - 1];
 #pragma unroll
-  for (int i = kPolyTerms - 2; i >= 0; --i) p = fma(p, r, poly_coef(i));
+  for (int i = kPolyTerms - 2; i >= 0; --i) p = fma(p, r, c_poly[i]);
   const double y = fma(p, r, 1.0);
   return y * __hiloint2double(hi, lo);
 }

@@ -156,15 +156,15 @@ std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g) 
 }
 
 int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
-               std::vector<Item>& items) {
+               int kBI, std::vector<Item>& items) {
   items.clear();
   const int npad = (n + kBJ - 1) / kBJ * kBJ;
   const int ntiles = npad / kBJ;
   const int nblocks = (re - rb + kBI - 1) / kBI;
   // Enough items to keep every SM busy for many waves (148 SMs x 4 CTAs x
-  // 16) and none larger than ~2^24 pair terms, capped at one tile each.
+  // 16) and none larger than ~2^25 pair terms, capped at one tile each.
   const double pairs_per_block = static_cast<double>(std::min(kBI, re - rb)) * n;
-  int slots = static_cast<int>(std::ceil(pairs_per_block / double(1 << 24)));
+  int slots = static_cast<int>(std::ceil(pairs_per_block / double(1 << 25)));
   slots = std::max(slots, (148 * 4 * 16 + nblocks - 1) / nblocks);
   slots = std::max(1, std::min(slots, ntiles));
   const int per = (ntiles + slots - 1) / slots;

@@ -39,11 +39,11 @@ constexpr double kCostAlpha = 13.0;  // FP64 instructions per background pair
 constexpr double kCostBeta = 17.0;   // FP64 instructions per trigger pair
 std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g);
 
-// Work items for rows [rb, re) of an n-event catalog: row blocks of kBI
-// rows times column chunks of whole tiles; heaviest first.  Returns the
+// Work items for rows [rb, re) of an n-event catalog: row blocks of
+// rows_per_item rows times column chunks of whole tiles; heaviest first.  Returns the
 // number of chunk slots per row.
 int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
-               std::vector<Item>& items);
+               int rows_per_item, std::vector<Item>& items);
 
 // Per-evaluation coefficients (types.hpp:105-109, model.hpp:328-336) and
 // the host-side argument bound that selects the checked exp.

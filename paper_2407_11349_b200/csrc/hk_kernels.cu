@@ -177,16 +177,16 @@ __device__ __forceinline__ void issue_tile(int type, int J, double* buf, uint64_
     if (mask & (1u << s)) bulk_g2s(buf + s * kBJ, src[s] + j0, kBytes, bar);
 }
 
+template <int R>
 struct RowState {
-  double t[kRowsPerThread], x[kRowsPerThread], y[kRowsPerThread];
-  int lb[kRowsPerThread], ub[kRowsPerThread];
-  double B[kRowsPerThread], B2[kRowsPerThread], T[kRowsPerThread], Td[kRowsPerThread],
-      Tq[kRowsPerThread];
+  double t[R], x[R], y[R];
+  int lb[R], ub[R];
+  double B[R], B2[R], T[R], Td[R], Tq[R];
 };
 
 // BT / B / T tiles: no per-pair guards.
-template <bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr>
-__device__ __forceinline__ void tile_fast(RowState& R, const double* __restrict__ buf,
+template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr>
+__device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restrict__ buf,
                                           const EvalCoef& c) {
   const double* __restrict__ st = buf + sT * kBJ;
   const double* __restrict__ sx = buf + sX * kBJ;
@@ -197,16 +197,16 @@ __device__ __forceinline__ void tile_fast(RowState& R, const double* __restrict_
   const double* __restrict__ sk = buf + sK * kBJ;
   const double* __restrict__ sthr = buf + sAux * kBJ;
   const double Kb = c.Kb, Kq0 = c.Kq0;
-  double Tp[kRowsPerThread], Vp[kRowsPerThread], Qp[kRowsPerThread];
+  double Tp[NR], Vp[NR], Qp[NR];
 #pragma unroll
-  for (int r = 0; r < kRowsPerThread; ++r) Tp[r] = Vp[r] = Qp[r] = 0.0;
+  for (int r = 0; r < NR; ++r) Tp[r] = Vp[r] = Qp[r] = 0.0;
 
 #pragma unroll kUnroll
   for (int j = 0; j < kBJ; ++j) {
     if (kBg) {
       const double tj = st[j];
 #pragma unroll
-      for (int r = 0; r < kRowsPerThread; ++r) {
+      for (int r = 0; r < NR; ++r) {
         const double td = R.t[r] - tj;
         const double td2 = td * td;
         const double b = exp2_16<kMode>(td2, Kb);
@@ -217,34 +217,29 @@ __device__ __forceinline__ void tile_fast(RowState& R, const double* __restrict_
     if (kTr) {
       const double xj = sx[j], yj = sy[j], wj = sw[j];
       const double Kj = kVarying ? sk[j] : Kq0;
-      double d2[kRowsPerThread];
+      double d2[NR];
 #pragma unroll
-      for (int r = 0; r < kRowsPerThread; ++r) {
+      for (int r = 0; r < NR; ++r) {
         const double dx = R.x[r] - xj, dy = R.y[r] - yj;
         d2[r] = fma(dx, dx, dy * dy);
       }
-      bool go = true;
-      if (kVarying) {
-        // Warp-uniform skip when every lane's spatial factor flushes to 0
-        // (d^2 above the per-source threshold; high-word integer compare
-        // of non-negative doubles is order-preserving and conservative).
-        const int thr_hi = __double2hiint(sthr[j]);
-        bool live = false;
+      const double vj = kGrad ? sv[j] : 0.0;
+      const double zj = kGrad ? (kVarying ? sz[j] : wj) : 0.0;
+      const int thr_hi = kVarying ? __double2hiint(sthr[j]) : 0;
 #pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) live |= __double2hiint(d2[r]) <= thr_hi;
-        go = __any_sync(0xffffffffu, live);
-      }
-      if (go) {
-        const double vj = kGrad ? sv[j] : 0.0;
-        const double zj = kGrad ? (kVarying ? sz[j] : wj) : 0.0;
-#pragma unroll
-        for (int r = 0; r < kRowsPerThread; ++r) {
-          const double e = exp2_16<kMode>(d2[r], Kj);
-          Tp[r] = fma(wj, e, Tp[r]);
-          if (kGrad) {
-            Vp[r] = fma(vj, e, Vp[r]);
-            Qp[r] = fma(zj, d2[r] * e, Qp[r]);
-          }
+      for (int r = 0; r < NR; ++r) {
+        if (kVarying) {
+          // Warp-uniform skip, per row slot (32 rows), when every lane's
+          // spatial factor flushes to 0: d^2 above the per-source threshold
+          // (high-word integer compare of non-negative doubles is
+          // order-preserving and conservative), so skipping is exact.
+          if (!__any_sync(0xffffffffu, __double2hiint(d2[r]) <= thr_hi)) continue;
+        }
+        const double e = exp2_16<kMode>(d2[r], Kj);
+        Tp[r] = fma(wj, e, Tp[r]);
+        if (kGrad) {
+          Vp[r] = fma(vj, e, Vp[r]);
+          Qp[r] = fma(zj, d2[r] * e, Qp[r]);
         }
       }
     }
@@ -252,7 +247,7 @@ __device__ __forceinline__ void tile_fast(RowState& R, const double* __restrict_
   if (kTr) {
     const double t_ref = st[kBJ - 1];
 #pragma unroll
-    for (int r = 0; r < kRowsPerThread; ++r) {
+    for (int r = 0; r < NR; ++r) {
       const double dt = R.t[r] - t_ref;  // >= 0 on BT/T tiles
       const double E = exp2_16<kMode>(dt, c.Kw);
       R.T[r] = fma(E, Tp[r], R.T[r]);
@@ -265,8 +260,8 @@ __device__ __forceinline__ void tile_fast(RowState& R, const double* __restrict_
 }
 
 // Background of a whole BTx/Bx tile by the block expansion (see kXP).
-template <bool kGrad>
-__device__ __forceinline__ void bg_expansion(RowState& R, const double* __restrict__ st,
+template <int NR, bool kGrad>
+__device__ __forceinline__ void bg_expansion(RowState<NR>& R, const double* __restrict__ st,
                                              const BlockInfo& bi, const EvalCoef& c,
                                              double (*s_red)[kNM]) {
   const double s = c.u_scale;
@@ -303,7 +298,7 @@ __device__ __forceinline__ void bg_expansion(RowState& R, const double* __restri
     m[n] = a;
   }
 #pragma unroll
-  for (int r = 0; r < kRowsPerThread; ++r) {
+  for (int r = 0; r < NR; ++r) {
     const double alpha = s * (R.t[r] - cI);
     const double gamma = D + alpha;
     const double x = 2.0 * alpha;
@@ -324,8 +319,8 @@ __device__ __forceinline__ void bg_expansion(RowState& R, const double* __restri
 }
 
 // M tiles: the reference's exact value guards, per pair.
-template <bool kVarying, bool kGrad, int kMode>
-__device__ __forceinline__ void tile_masked(RowState& R, int j0, int n,
+template <int NR, bool kVarying, bool kGrad, int kMode>
+__device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
                                             const double* __restrict__ buf, const EvalCoef& c) {
   const double* __restrict__ st = buf + sT * kBJ;
   const double* __restrict__ sx = buf + sX * kBJ;
@@ -340,7 +335,7 @@ __device__ __forceinline__ void tile_masked(RowState& R, int j0, int n,
     const double qj = kVarying ? sq[j] : 1.0;
     const double Kj = kVarying ? sk[j] : Kq0;
 #pragma unroll
-    for (int r = 0; r < kRowsPerThread; ++r) {
+    for (int r = 0; r < NR; ++r) {
       const double td = R.t[r] - tj;
       const double td2 = td * td;
       double b = exp2_16<kMode>(td2, Kb);
@@ -364,7 +359,9 @@ __device__ __forceinline__ void tile_masked(RowState& R, int j0, int n,
 }
 
 template <bool kVarying, bool kGrad, int kMode>
-__global__ void __launch_bounds__(kThreads, HK_MIN_BLOCKS) pair_kernel(const PairParams P) {
+__global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)))
+    pair_kernel(const PairParams P) {
+  constexpr int NR = rows_per_thread(kVarying);
   __shared__ __align__(128) double s_buf[2][kSlots * kBJ];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ double s_red[kThreads / 32][kNM];
@@ -386,10 +383,10 @@ __global__ void __launch_bounds__(kThreads, HK_MIN_BLOCKS) pair_kernel(const Pai
   bi.t_first = P.d.t[it.rb];
   bi.t_last = P.d.t[it.re - 1];
 
-  RowState R;
-  bool valid[kRowsPerThread];
+  RowState<NR> R;
+  bool valid[NR];
 #pragma unroll
-  for (int r = 0; r < kRowsPerThread; ++r) {
+  for (int r = 0; r < NR; ++r) {
     int row = it.rb + tid + r * kThreads;
     valid[r] = row < it.re;
     row = valid[r] ? row : it.re - 1;
@@ -422,23 +419,23 @@ __global__ void __launch_bounds__(kThreads, HK_MIN_BLOCKS) pair_kernel(const Pai
     const double* buf = s_buf[stage];
     switch (tile_type(cur, bi, P)) {
       case kTileBT:
-        tile_fast<kVarying, kGrad, kMode, true, true>(R, buf, P.c);
+        tile_fast<NR, kVarying, kGrad, kMode, true, true>(R, buf, P.c);
         break;
       case kTileB:
-        tile_fast<kVarying, kGrad, kMode, true, false>(R, buf, P.c);
+        tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, P.c);
         break;
       case kTileT:
-        tile_fast<kVarying, kGrad, kMode, false, true>(R, buf, P.c);
+        tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, P.c);
         break;
       case kTileBTx:
-        bg_expansion<kGrad>(R, buf + sT * kBJ, bi, P.c, s_red);
-        tile_fast<kVarying, kGrad, kMode, false, true>(R, buf, P.c);
+        bg_expansion<NR, kGrad>(R, buf + sT * kBJ, bi, P.c, s_red);
+        tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, P.c);
         break;
       case kTileBx:
-        bg_expansion<kGrad>(R, buf + sT * kBJ, bi, P.c, s_red);
+        bg_expansion<NR, kGrad>(R, buf + sT * kBJ, bi, P.c, s_red);
         break;
       default:
-        tile_masked<kVarying, kGrad, kMode>(R, cur * kBJ, P.d.n, buf, P.c);
+        tile_masked<NR, kVarying, kGrad, kMode>(R, cur * kBJ, P.d.n, buf, P.c);
         break;
     }
     __syncthreads();  // every warp is done with this stage before it is refilled
@@ -449,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, HK_MIN_BLOCKS) pair_kernel(const Pai
   const size_t plane = static_cast<size_t>(P.rows_total);
   double* out = P.partial + static_cast<size_t>(it.slot) * 5 * plane;
 #pragma unroll
-  for (int r = 0; r < kRowsPerThread; ++r) {
+  for (int r = 0; r < NR; ++r) {
     if (!valid[r]) continue;
     const size_t i = static_cast<size_t>(it.rb + tid + r * kThreads - P.rows_base);
     out[0 * plane + i] = R.B[r];
