@@ -3,8 +3,9 @@
 // Per evaluation (one stream, four launches):
 //   1. prep   O(N)    per-source trigger coefficients, tile-relative temporal
 //                     weights w_j, and the skip thresholds.
-//   2. pair   O(N^2)  one CTA per work item (256 rows x a range of 256-column
-//                     tiles).  Rows live in registers (2 per thread); column
+//   2. pair   O(N^2)  one CTA per work item (512 rows constant / 256 varying x
+//                     a range of 256-column tiles).  Rows live in registers
+//                     (4 / 2 per thread); column
 //                     tiles are staged in shared memory with bulk-async
 //                     copies (cp.async.bulk + mbarrier, double-buffered).
 //                     Five FP64 accumulators per row:
@@ -32,6 +33,8 @@
 //   M   the band around the rows' own times: per-pair guards
 //       t_j != t_i (as j outside [lb_i, ub_i)) and t_j < t_i (j < lb_i),
 //       exactly the reference's value guards (model.hpp:263, :278).
+//   BTx/Bx  BT/B tiles whose background is evaluated by the exact block
+//       expansion (kXP below) instead of per pair.
 //   skip tiles whose every term flushes to zero in this arithmetic.
 #include <cuda_runtime.h>
 
