@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--n", type=int, default=1_000_000)
     ap.add_argument("--variant", choices=["constant", "varying"], default="constant")
     ap.add_argument("--cpu-rows", type=int, default=CPU_SAMPLE_ROWS)
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the torch.distributed/NCCL row-shard path even with one rank")
     return ap.parse_args()
 
 
@@ -195,12 +197,13 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     cat = benchmark_catalog(args.n, 42)
     p = HawkesParams(**BENCH_PARAMS, variant=Variant[args.variant])
-    if world > 1:
+    if use_dist:
         sh = ShardedLikelihood(cat, device=local)
         ev, stream = sh.ev, sh.stream
     else:
@@ -229,7 +232,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev.reset_profile()
     ev.set_profiling(True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local) if rank == 0 else None
@@ -241,14 +244,14 @@ def run_ours(args):
     with torch.cuda.stream(stream):
         e1.record()
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     clk = clocks.stop() if clocks else None
     ms_total = e0.elapsed_time(e1)
     pair_ms, pair_launches, launches = ev.profile()
     ev.set_profiling(False)
     t = torch.tensor([ms_total, pair_ms / max(pair_launches, 1)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, pair_ms_avg = float(t[0]), float(t[1])
     # result of the last step, for the record
@@ -271,14 +274,14 @@ def run_ours(args):
         return ev.eval(p, grad=True)
 
     e2e_step()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         e2e_step()
     e2e_s = time.perf_counter() - t0
     t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_s = float(t[0])
 
