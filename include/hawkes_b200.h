@@ -12,8 +12,8 @@
  *   event_contribution          model.hpp:351-356  hk_eval_rows(b, b+1)
  *   LikelihoodWorkspace<double>::set_locations     hk_set_locations
  *                               engine.hpp:172-178
- *   LikelihoodWorkspace<double>::evaluate_*        hk_eval (full O(N^2) pass)
- *                               engine.hpp:133-158
+ *   LikelihoodWorkspace<double>::evaluate_*        hk_ws_eval (device-cached
+ *                               engine.hpp:133-158   row sums per half)
  *   Partition::make             engine.hpp:27-40   hk_partition_make
  *   benchmark_catalog           engine.hpp:251-259 hk_benchmark_catalog
  *   (new, no reference counterpart)                hk_eval with grad5 != NULL,
@@ -96,6 +96,18 @@ int hk_set_locations_device(hk_ctx* ctx, const double* lon_device, const double*
  * rows of ell_n, engine.hpp:65-99 / model.hpp:340-349).  If grad5 != NULL it
  * receives d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t).  Synchronous. */
 int hk_eval(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5);
+
+/* Workspace evaluation (LikelihoodWorkspace<double>, engine.hpp:117-229):
+ * like hk_eval, but the per-row background sums [B, B2] are reused while
+ * tau_t is unchanged and the trigger sums [T, Td, Tq] while sigma_x,
+ * sigma_t, the variant and the locations are unchanged (two cached states
+ * per half: current + proposal).  A mu0/xi0 proposal is an O(N)
+ * recombination; tau_t refreshes only the background; sigma_x/sigma_t or
+ * hk_set_locations only the trigger.  force != 0 recomputes both halves
+ * (evaluate_full).  Results are bitwise identical to hk_eval's. */
+int hk_ws_eval(hk_ctx* ctx, const hk_params* p, int force, double* ll, double* grad5);
+/* Cache hits / misses of hk_ws_eval since creation. */
+int hk_ws_stats(const hk_ctx* ctx, long* hits, long* misses);
 
 /* Asynchronous form: enqueues the evaluation on the context's stream and
  * leaves [ll, g_mu0, g_tau_t, g_xi0, g_sigma_x, g_sigma_t] in a device buffer

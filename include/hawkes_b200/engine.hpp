@@ -101,6 +101,14 @@ class Engine {
     detail::check(hk_set_locations(ctx_.get(), lon.data(), lat.data()));
   }
 
+  // Device-cached workspace evaluation (hk_ws_eval).
+  double workspace_eval(const HawkesParams& p, Variant v, bool force, double* grad5 = nullptr) {
+    const hk_params c = detail::to_c(p, v);
+    double ll = 0.0;
+    detail::check(hk_ws_eval(ctx_.get(), &c, force ? 1 : 0, &ll, grad5));
+    return ll;
+  }
+
  private:
   std::unique_ptr<hk_ctx, void (*)(hk_ctx*)> ctx_;
 };
@@ -137,8 +145,10 @@ inline double event_contribution(const HawkesParams& p, const Catalog& catalog, 
 }
 
 /// LikelihoodWorkspace<Real> (engine.hpp:117-229): same constructor and
-/// methods; every evaluation is one full device pass (the device-resident
-/// lane caches are the next step).
+/// methods.  The per-row background [B, B2] and trigger [T, Td, Tq] sums are
+/// cached on the device (hk_ws_eval): mu0/xi0 proposals recombine in O(N),
+/// tau_t refreshes only the background, sigma_x/sigma_t and set_locations
+/// only the trigger; results are bitwise identical to a full evaluation.
 template <typename Real>
 class LikelihoodWorkspace {
   // Precision::single (Real = float) is rejected at construction, like
@@ -157,23 +167,24 @@ class LikelihoodWorkspace {
 
   double evaluate_full(const HawkesParams& p) {
     current_ = p;
-    return engine_.log_likelihood(p, variant_);
+    return engine_.workspace_eval(p, variant_, /*force=*/true);
   }
 
   double evaluate_proposal(const HawkesParams& p) {
     proposal_ = p;
-    return engine_.log_likelihood(p, variant_);
+    return engine_.workspace_eval(p, variant_, /*force=*/false);
   }
 
+  // Both the current and the proposal state stay cached on the device.
   void commit_proposal() { current_ = proposal_; }
 
   void set_locations(const std::vector<double>& lon, const std::vector<double>& lat) {
     engine_.set_locations(lon, lat);
   }
 
-  double evaluate_full_with_gradient(const HawkesParams& p, std::array<double, 5>& grad) {
+  double evaluate_with_gradient(const HawkesParams& p, std::array<double, 5>& grad) {
     current_ = p;
-    return engine_.log_likelihood_and_gradient(p, variant_, grad);
+    return engine_.workspace_eval(p, variant_, /*force=*/false, grad.data());
   }
 
  private:

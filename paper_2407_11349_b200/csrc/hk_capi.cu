@@ -78,6 +78,8 @@ struct DeviceState {
   hk::Item* items[2] = {nullptr, nullptr};
   int n_items[2] = {0, 0}, slots[2] = {0, 0};
   double* partial = nullptr;
+  double* bg_sums[2] = {nullptr, nullptr};  // [B, B2] x rows, LRU-2 (workspace cache)
+  double* tr_sums[2] = {nullptr, nullptr};  // [T, Td, Tq] x rows
   double* blockpart = nullptr;
   int n_finish_blocks = 0;
   double* out6 = nullptr;
@@ -101,6 +103,24 @@ struct hk_ctx {
   std::vector<DeviceState> devs;
   bool profiling = false;
   int bg_expansion = 1;
+
+  // Workspace cache keys (LikelihoodWorkspace semantics, engine.hpp:117-229):
+  // the background half depends on tau_t only, the trigger half on
+  // (sigma_x, sigma_t, variant) and the locations.  Two entries per half
+  // hold the current state and a proposal; the least recently used is
+  // replaced.  Every evaluation goes through the same kernels, so cached and
+  // fresh results are bitwise identical.
+  struct Key {
+    bool valid = false;
+    double a = 0, b = 0;
+    int variant = 0, grad = 0, bgx = 0;
+    long loc = 0;
+    unsigned long long used = 0;
+  };
+  Key bg_key[2], tr_key[2];
+  long loc_version = 0;
+  unsigned long long clock = 0;
+  long ws_hits = 0, ws_misses = 0;
   double prof_ms = 0.0;
   long prof_pair = 0, prof_total = 0;
 
@@ -108,7 +128,8 @@ struct hk_ctx {
     for (auto& s : devs) {
       cudaSetDevice(s.dev);
       if (s.stream) cudaStreamSynchronize(s.stream);
-      for (double* p : {s.t, s.x, s.y, s.q, s.K, s.thr, s.w, s.v, s.z, s.partial, s.blockpart, s.out6})
+      for (double* p : {s.t, s.x, s.y, s.q, s.K, s.thr, s.w, s.v, s.z, s.partial, s.blockpart, s.out6,
+                        s.bg_sums[0], s.bg_sums[1], s.tr_sums[0], s.tr_sums[1]})
         if (p) cudaFree(p);
       if (s.lb) cudaFree(s.lb);
       if (s.ub) cudaFree(s.ub);
@@ -177,6 +198,10 @@ struct hk_ctx {
     }
     const std::size_t rows = static_cast<std::size_t>(re - rb);
     s.partial = dmalloc<double>(static_cast<std::size_t>(std::max(s.slots[0], s.slots[1])) * 5 * rows);
+    for (int k = 0; k < 2; ++k) {
+      s.bg_sums[k] = dmalloc<double>(2 * rows);
+      s.tr_sums[k] = dmalloc<double>(3 * rows);
+    }
     s.n_finish_blocks = static_cast<int>((rows + 255) / 256);
     s.blockpart = dmalloc<double>(static_cast<std::size_t>(s.n_finish_blocks) * 6);
     s.out6 = dmalloc<double>(6);
@@ -206,25 +231,88 @@ struct hk_ctx {
     return c;
   }
 
-  // Enqueues prep + pair + finish + reduce for device s.
-  void enqueue(DeviceState& s, const hk::EvalCoef& c, bool grad) {
+  // Picks the cache entry for each half: a hit (unless forced) or the least
+  // recently used entry, which the next enqueue recomputes.  Returns the
+  // halves to compute.
+  int plan_halves(const hk::EvalCoef& c, bool grad, bool force, int& bgi, int& tri) {
+    auto hit_bg = [&](const Key& k) {
+      return k.valid && k.a == c.tau_t && k.bgx == c.bg_expansion && (k.grad || !grad);
+    };
+    auto hit_tr = [&](const Key& k) {
+      return k.valid && k.a == c.sigma_x && k.b == c.sigma_t && k.variant == c.varying &&
+             k.loc == loc_version && (k.grad || !grad);
+    };
+    int halves = 0;
+    bgi = -1;
+    tri = -1;
+    if (!force)
+      for (int k = 0; k < 2; ++k) {
+        if (bgi < 0 && hit_bg(bg_key[k])) bgi = k;
+        if (tri < 0 && hit_tr(tr_key[k])) tri = k;
+      }
+    if (bgi < 0) {
+      halves |= hk::kHalfBg;
+      bgi = bg_key[0].used <= bg_key[1].used ? 0 : 1;
+      bg_key[bgi] = Key{true, c.tau_t, 0, 0, grad ? 1 : 0, c.bg_expansion, 0, 0};
+    }
+    if (tri < 0) {
+      halves |= hk::kHalfTr;
+      tri = tr_key[0].used <= tr_key[1].used ? 0 : 1;
+      tr_key[tri] = Key{true, c.sigma_x, c.sigma_t, c.varying, grad ? 1 : 0, 0, loc_version, 0};
+    }
+    bg_key[bgi].used = ++clock;
+    tr_key[tri].used = ++clock;
+    if (halves) ++ws_misses; else ++ws_hits;
+    return halves;
+  }
+
+  // Enqueues [prep + pair + collapse for the missing halves] + finish + reduce.
+  void enqueue(DeviceState& s, const hk::EvalCoef& c, bool grad, int halves, int bgi, int tri) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const hk::DeviceCatalog dc = s.catalog(n, npad);
-    hk::launch_prep(dc, c, s.stream);
-    std::pair<cudaEvent_t, cudaEvent_t> ev{};
-    if (profiling) {
-      ev = next_events(s);
-      ck(cudaEventRecord(ev.first, s.stream), "cudaEventRecord");
+    const int rows = s.re - s.rb;
+    if (halves) {
+      hk::launch_prep(dc, c, s.stream);
+      std::pair<cudaEvent_t, cudaEvent_t> ev{};
+      if (profiling) {
+        ev = next_events(s);
+        ck(cudaEventRecord(ev.first, s.stream), "cudaEventRecord");
+      }
+      const int v = c.varying ? 1 : 0;
+      hk::launch_pair(dc, c, s.items[v], s.n_items[v], s.partial, s.rb, rows, grad, halves, s.stream);
+      if (profiling) ck(cudaEventRecord(ev.second, s.stream), "cudaEventRecord");
+      hk::launch_collapse(s.partial, s.slots[v], rows, (halves & hk::kHalfBg) ? s.bg_sums[bgi] : nullptr,
+                          (halves & hk::kHalfTr) ? s.tr_sums[tri] : nullptr, s.stream);
+      if (profiling) prof_pair += 1;
+      prof_total += 3;
     }
-    const int v = c.varying ? 1 : 0;
-    hk::launch_pair(dc, c, s.items[v], s.n_items[v], s.partial, s.rb, s.re - s.rb, grad, s.stream);
-    if (profiling) ck(cudaEventRecord(ev.second, s.stream), "cudaEventRecord");
-    hk::launch_finish(dc, c, s.partial, s.slots[v], s.rb, s.re - s.rb, grad, nullptr, nullptr,
+    hk::launch_finish(dc, c, s.bg_sums[bgi], s.tr_sums[tri], s.rb, rows, grad, nullptr, nullptr,
                       s.blockpart, s.stream);
     hk::launch_reduce(s.blockpart, s.n_finish_blocks, s.out6, s.stream);
     ck(cudaGetLastError(), "kernel launch");
-    if (profiling) prof_pair += 1;
-    prof_total += 4;
+    prof_total += 2;
+  }
+
+  // Full or workspace evaluation on every device; sums in device order.
+  void evaluate(const hk_params* p, bool grad, bool workspace, bool force, double* ll, double* grad5) {
+    const hk::EvalCoef c = coef(p);
+    int bgi, tri;
+    const int halves = workspace ? plan_halves(c, grad, force, bgi, tri)
+                                 : plan_halves(c, grad, /*force=*/true, bgi, tri);
+    for (auto& s : devs) {
+      enqueue(s, c, grad, halves, bgi, tri);
+      ck(cudaMemcpyAsync(s.h_out6, s.out6, 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
+         "result copy");
+    }
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    for (auto& s : devs) {  // device order: deterministic
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaStreamSynchronize(s.stream), "hk_eval");
+      for (int k = 0; k < 6; ++k) acc[k] += s.h_out6[k];
+    }
+    *ll = acc[0];
+    if (grad5)
+      for (int k = 0; k < 5; ++k) grad5[k] = acc[1 + k];
   }
 };
 
@@ -305,6 +393,7 @@ int hk_set_locations(hk_ctx* ctx, const double* lon, const double* lat) {
     std::copy(lon, lon + ctx->n, ctx->x.begin());
     std::copy(lat, lat + ctx->n, ctx->y.begin());
     ctx->update_bbox();
+    ++ctx->loc_version;  // drops the trigger caches (engine.hpp:177)
     for (auto& s : ctx->devs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       ck(cudaMemcpyAsync(s.x, lon, ctx->n * sizeof(double), cudaMemcpyHostToDevice, s.stream),
@@ -336,28 +425,29 @@ int hk_set_locations_device(hk_ctx* ctx, const double* lon_device, const double*
        "mirror");
     ck(cudaStreamSynchronize(s.stream), "mirror sync");
     ctx->update_bbox();
+    ++ctx->loc_version;
   });
 }
 
 int hk_eval(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5) {
   return guarded([&] {
     if (!ctx || !ll) throw std::invalid_argument("hk_eval: null argument");
-    const hk::EvalCoef c = ctx->coef(p);
-    const bool grad = grad5 != nullptr;
-    for (auto& s : ctx->devs) {
-      ctx->enqueue(s, c, grad);
-      ck(cudaMemcpyAsync(s.h_out6, s.out6, 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
-         "result copy");
-    }
-    double acc[6] = {0, 0, 0, 0, 0, 0};
-    for (auto& s : ctx->devs) {  // device order: deterministic
-      ck(cudaSetDevice(s.dev), "cudaSetDevice");
-      ck(cudaStreamSynchronize(s.stream), "hk_eval");
-      for (int k = 0; k < 6; ++k) acc[k] += s.h_out6[k];
-    }
-    *ll = acc[0];
-    if (grad5)
-      for (int k = 0; k < 5; ++k) grad5[k] = acc[1 + k];
+    ctx->evaluate(p, grad5 != nullptr, /*workspace=*/false, /*force=*/true, ll, grad5);
+  });
+}
+
+int hk_ws_eval(hk_ctx* ctx, const hk_params* p, int force, double* ll, double* grad5) {
+  return guarded([&] {
+    if (!ctx || !ll) throw std::invalid_argument("hk_ws_eval: null argument");
+    ctx->evaluate(p, grad5 != nullptr, /*workspace=*/true, force != 0, ll, grad5);
+  });
+}
+
+int hk_ws_stats(const hk_ctx* ctx, long* hits, long* misses) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("hk_ws_stats: null context");
+    if (hits) *hits = ctx->ws_hits;
+    if (misses) *misses = ctx->ws_misses;
   });
 }
 
@@ -367,7 +457,9 @@ int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad) {
     if (ctx->devs.size() != 1)
       throw std::invalid_argument("hk_eval_async: single-device contexts only");
     const hk::EvalCoef c = ctx->coef(p);
-    ctx->enqueue(ctx->devs[0], c, with_grad != 0);
+    int bgi, tri;
+    const int halves = ctx->plan_halves(c, with_grad != 0, /*force=*/true, bgi, tri);
+    ctx->enqueue(ctx->devs[0], c, with_grad != 0, halves, bgi, tri);
   });
 }
 
@@ -405,7 +497,9 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
     double* d_grad = dmalloc<double>(rows * 5);
     const int nfb = static_cast<int>((rows + 255) / 256);
     double* d_bp = dmalloc<double>(static_cast<std::size_t>(nfb) * 6);
+    double* d_sums = dmalloc<double>(5 * rows);
     auto cleanup = [&] {
+      cudaFree(d_sums);
       cudaFree(d_items);
       cudaFree(d_partial);
       cudaFree(d_ell);
@@ -420,11 +514,12 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
       hk::launch_prep(dc, c, s.stream);
       const bool grad = grad_rows != nullptr;
       hk::launch_pair(dc, c, d_items, static_cast<int>(items.size()), d_partial, rb, re - rb, grad,
-                      s.stream);
-      hk::launch_finish(dc, c, d_partial, slots, rb, re - rb, grad, d_ell, grad ? d_grad : nullptr,
-                        d_bp, s.stream);
+                      hk::kHalfBg | hk::kHalfTr, s.stream);
+      hk::launch_collapse(d_partial, slots, re - rb, d_sums, d_sums + 2 * rows, s.stream);
+      hk::launch_finish(dc, c, d_sums, d_sums + 2 * rows, rb, re - rb, grad, d_ell,
+                        grad ? d_grad : nullptr, d_bp, s.stream);
       ck(cudaGetLastError(), "kernel launch");
-      ctx->prof_total += 3;
+      ctx->prof_total += 4;
       ck(cudaMemcpyAsync(ell_rows, d_ell, rows * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
          "rows copy");
       if (grad)

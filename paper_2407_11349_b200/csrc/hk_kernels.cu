@@ -119,6 +119,7 @@ struct PairParams {
   const Item* items;
   double* partial;
   int rows_base, rows_total;
+  int halves;  // kHalfBg | kHalfTr: which row sums this launch must produce
 };
 
 struct BlockInfo {
@@ -135,7 +136,25 @@ __device__ __forceinline__ bool expansion_ok(const BlockInfo& bi, double t0, dou
   return 2.0 * hI * hJ <= kEpsMax && 2.0 * fabs(D) * hJ <= kDBetaMax;
 }
 
+__device__ __forceinline__ int tile_type_all(int J, const BlockInfo& bi, const PairParams& P);
+
+// Tile class restricted to the requested halves (workspace refreshes): a
+// background-only launch turns BT/BTx into B/Bx and skips T tiles; a
+// trigger-only launch turns BT/BTx into T and skips B/Bx tiles.  M tiles
+// compute both halves (one per row block; the unused half is discarded).
 __device__ __forceinline__ int tile_type(int J, const BlockInfo& bi, const PairParams& P) {
+  const int t = tile_type_all(J, bi, P);
+  if (P.halves == (kHalfBg | kHalfTr) || t == kTileM || t == kSkip) return t;
+  if (P.halves == kHalfBg) {
+    if (t == kTileBT) return kTileB;
+    if (t == kTileBTx) return kTileBx;
+    return t == kTileT ? kSkip : t;
+  }
+  if (t == kTileBT || t == kTileBTx) return kTileT;
+  return (t == kTileB || t == kTileBx) ? kSkip : t;
+}
+
+__device__ __forceinline__ int tile_type_all(int J, const BlockInfo& bi, const PairParams& P) {
   const int j0 = J * kBJ, j1 = j0 + kBJ;
   const double* __restrict__ t = P.d.t;
   if (j1 <= bi.lbmin) {
@@ -156,19 +175,24 @@ __device__ __forceinline__ int tile_type(int J, const BlockInfo& bi, const PairP
 }
 
 template <bool kVarying, bool kGrad>
-__device__ __forceinline__ void issue_tile(int type, int J, double* buf, uint64_t* bar,
+__device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf, uint64_t* bar,
                                            const PairParams& P) {
   const int j0 = J * kBJ;
   constexpr unsigned kBytes = kBJ * sizeof(double);
+  if (type == kTileBx) {  // a group of cnt background-only tiles: their times, contiguous
+    mbar_expect_tx(bar, kBytes * cnt);
+    bulk_g2s(buf, P.d.t + j0, kBytes * cnt, bar);
+    return;
+  }
   unsigned mask = 0;
-  if (type == kTileB || type == kTileBx) {
+  if (type == kTileB) {
     mask = 1u << sT;
   } else if (type == kTileM) {
     mask = (1u << sT) | (1u << sX) | (1u << sY);
     if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = q
   } else {  // BT, BTx or T
     mask = (1u << sT) | (1u << sX) | (1u << sY) | (1u << sW);
-    if (kGrad) mask |= (1u << sV) | (1u << sZ);
+    if (kGrad) mask |= (1u << sV);
     if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = thr
     if (kVarying && kGrad) mask |= (1u << sZ);
   }
@@ -262,43 +286,54 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
   }
 }
 
-// Background of a whole BTx/Bx tile by the block expansion (see kXP).
-template <int NR, bool kGrad>
+// Background of ncols staged columns (one BTx tile or a group of Bx tiles)
+// by the block expansion (see kXP).  The number of Taylor terms adapts to
+// eps so the remainder stays below 2^-64 relative.
+template <int NR, bool kGrad, int kMode>
 __device__ __forceinline__ void bg_expansion(RowState<NR>& R, const double* __restrict__ st,
-                                             const BlockInfo& bi, const EvalCoef& c,
+                                             int ncols, const BlockInfo& bi, const EvalCoef& c,
                                              double (*s_red)[kNM]) {
   const double s = c.u_scale;
   const double cI = 0.5 * (bi.t_first + bi.t_last);
-  const double cJ = 0.5 * (st[0] + st[kBJ - 1]);
+  const double cJ = 0.5 * (st[0] + st[ncols - 1]);
   const double D = s * (cI - cJ);
+  const double eps = 0.5 * s * s * (bi.t_last - bi.t_first) * (st[ncols - 1] - st[0]);
+  int P = 2;  // smallest number of terms with eps^(P+1)/(P+1)! <= 2^-64 (uniform)
+  for (double rem = eps * eps * eps / 6.0; P < kXP && rem > 5.421010862427522e-20; ++P)
+    rem *= eps / (P + 2);
+  const int nm = P + (kGrad ? 3 : 1);
   double m[kNM];
 #pragma unroll
   for (int n = 0; n < kNM; ++n) m[n] = 0.0;
-  for (int jj = threadIdx.x; jj < kBJ; jj += kThreads) {
+  for (int jj = threadIdx.x; jj < ncols; jj += kThreads) {
     const double beta = s * (st[jj] - cJ);
-    double p = exp(fma(2.0 * D, beta, -beta * beta));  // column factor C_j
+    double p = exp2_16_arg<kMode>(fma(2.0 * D, beta, -beta * beta) * kLog2eT);  // C_j
 #pragma unroll
     for (int n = 0; n < kNM; ++n) {
-      m[n] += p;
+      if (n < nm) m[n] += p;
       p *= beta;
     }
   }
   // fixed-order reduction over the CTA: warp butterfly, then warps in order
 #pragma unroll
   for (int n = 0; n < kNM; ++n)
+    if (n < nm)
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m[n] += __shfl_xor_sync(0xffffffffu, m[n], off);
+      for (int off = 16; off > 0; off >>= 1) m[n] += __shfl_xor_sync(0xffffffffu, m[n], off);
   const int warp = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0)
 #pragma unroll
-    for (int n = 0; n < kNM; ++n) s_red[warp][n] = m[n];
+    for (int n = 0; n < kNM; ++n)
+      if (n < nm) s_red[warp][n] = m[n];
   __syncthreads();
 #pragma unroll
   for (int n = 0; n < kNM; ++n) {
-    double a = s_red[0][n];
+    if (n < nm) {
+      double a = s_red[0][n];
 #pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) a += s_red[w][n];
-    m[n] = a;
+      for (int w = 1; w < kThreads / 32; ++w) a += s_red[w][n];
+      m[n] = a;
+    }
   }
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
@@ -308,14 +343,23 @@ __device__ __forceinline__ void bg_expansion(RowState<NR>& R, const double* __re
     double S0 = m[kXP], S1 = m[kXP + 1], S2 = m[kXP + 2];
 #pragma unroll
     for (int n = kXP; n >= 1; --n) {
-      const double xn = x * (1.0 / n);
-      S0 = fma(xn, S0, m[n - 1]);
-      if (kGrad) {
-        S1 = fma(xn, S1, m[n]);
-        S2 = fma(xn, S2, m[n + 1]);
+      if (n == P) {  // start Horner at the last kept term
+        S0 = m[n];
+        if (kGrad) {
+          S1 = m[n + 1];
+          S2 = m[n + 2];
+        }
+      }
+      if (n <= P) {
+        const double xn = x * (1.0 / n);
+        S0 = fma(xn, S0, m[n - 1]);
+        if (kGrad) {
+          S1 = fma(xn, S1, m[n]);
+          S2 = fma(xn, S2, m[n + 1]);
+        }
       }
     }
-    const double Rf = exp(-gamma * gamma);  // row factor R_i
+    const double Rf = exp2_16_arg<kMode>(-gamma * gamma * kLog2eT);  // row factor R_i
     R.B[r] = fma(Rf, S0, R.B[r]);
     if (kGrad) R.B2[r] = fma(Rf * c.two_tau2, fma(gamma, fma(gamma, S0, -2.0 * S1), S2), R.B2[r]);
   }
@@ -402,25 +446,38 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
   }
   __syncthreads();
 
-  auto next_live = [&](int J) {
-    while (J < it.te && tile_type(J, bi, P) == kSkip) ++J;
-    return J;
+  // Work units: one tile, or a group of consecutive Bx (background-only,
+  // expansion) tiles evaluated as one expansion over up to kSlots*kBJ columns.
+  struct Unit {
+    int J, cnt, type;
+  };
+  auto unit_at = [&](int J) {
+    int ty = kSkip;
+    while (J < it.te && (ty = tile_type(J, bi, P)) == kSkip) ++J;
+    Unit u{J, J < it.te ? 1 : 0, ty};
+    // Grouping follows the full (both-halves) classification, so a
+    // background-only workspace refresh sums exactly like a full launch and
+    // cached results stay bitwise identical to fresh ones.
+    if (ty == kTileBx && tile_type_all(J, bi, P) == kTileBx)
+      while (u.cnt < kSlots && J + u.cnt < it.te && tile_type_all(J + u.cnt, bi, P) == kTileBx &&
+             expansion_ok(bi, P.d.t[J * kBJ], P.d.t[(J + u.cnt + 1) * kBJ - 1], P.c))
+        ++u.cnt;
+    return u;
   };
 
-  int cur = next_live(it.tb);
+  Unit cur = unit_at(it.tb);
   int stage = 0;
   unsigned phases = 0u;  // bit s = parity of the next wait on stage s
-  if (cur < it.te && tid == 0)
-    issue_tile<kVarying, kGrad>(tile_type(cur, bi, P), cur, s_buf[0], &s_bar[0], P);
-  while (cur < it.te) {
-    const int nxt = next_live(cur + 1);
-    if (nxt < it.te && tid == 0)
-      issue_tile<kVarying, kGrad>(tile_type(nxt, bi, P), nxt, s_buf[stage ^ 1], &s_bar[stage ^ 1],
-                                  P);
+  if (cur.cnt && tid == 0)
+    issue_tile<kVarying, kGrad>(cur.type, cur.J, cur.cnt, s_buf[0], &s_bar[0], P);
+  while (cur.cnt) {
+    const Unit nxt = unit_at(cur.J + cur.cnt);
+    if (nxt.cnt && tid == 0)
+      issue_tile<kVarying, kGrad>(nxt.type, nxt.J, nxt.cnt, s_buf[stage ^ 1], &s_bar[stage ^ 1], P);
     mbar_wait(&s_bar[stage], (phases >> stage) & 1u);
     phases ^= 1u << stage;
     const double* buf = s_buf[stage];
-    switch (tile_type(cur, bi, P)) {
+    switch (cur.type) {
       case kTileBT:
         tile_fast<NR, kVarying, kGrad, kMode, true, true>(R, buf, P.c);
         break;
@@ -431,14 +488,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
         tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, P.c);
         break;
       case kTileBTx:
-        bg_expansion<NR, kGrad>(R, buf + sT * kBJ, bi, P.c, s_red);
+        bg_expansion<NR, kGrad, kMode>(R, buf + sT * kBJ, kBJ, bi, P.c, s_red);
         tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, P.c);
         break;
       case kTileBx:
-        bg_expansion<NR, kGrad>(R, buf + sT * kBJ, bi, P.c, s_red);
+        bg_expansion<NR, kGrad, kMode>(R, buf, cur.cnt * kBJ, bi, P.c, s_red);
         break;
       default:
-        tile_masked<NR, kVarying, kGrad, kMode>(R, cur * kBJ, P.d.n, buf, P.c);
+        tile_masked<NR, kVarying, kGrad, kMode>(R, cur.J * kBJ, P.d.n, buf, P.c);
         break;
     }
     __syncthreads();  // every warp is done with this stage before it is refilled
@@ -491,6 +548,30 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
 
 constexpr int kFinishThreads = 256;
 
+// Per-row sums of the partial slots, in slot order (deterministic), into the
+// background [B, B2] and/or trigger [T, Td, Tq] planes.
+__global__ void collapse_kernel(const double* __restrict__ partial, int slots, int rows_total,
+                                double* bg_sums, double* tr_sums) {
+  const int li = blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= rows_total) return;
+  const size_t plane = static_cast<size_t>(rows_total);
+  double a[5] = {0, 0, 0, 0, 0};
+  for (int s = 0; s < slots; ++s) {
+    const double* p = partial + static_cast<size_t>(s) * 5 * plane + li;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) a[k] += p[k * plane];
+  }
+  if (bg_sums) {
+    bg_sums[li] = a[0];
+    bg_sums[plane + li] = a[1];
+  }
+  if (tr_sums) {
+    tr_sums[li] = a[2];
+    tr_sums[plane + li] = a[3];
+    tr_sums[2 * plane + li] = a[4];
+  }
+}
+
 __device__ __forceinline__ double gaussian_cdf(double z) {
   return 0.5 * erfc(-z * 0.7071067811865475244);  // model.hpp:157-160
 }
@@ -500,24 +581,17 @@ __device__ __forceinline__ double gaussian_pdf(double z) {
 }
 
 __global__ void __launch_bounds__(kFinishThreads) finish_kernel(
-    const DeviceCatalog d, const EvalCoef c, const double* __restrict__ partial, int slots,
-    int rows_base, int rows_total, int with_grad, double* ell_rows, double* grad_rows,
-    double* blockpart) {
+    const DeviceCatalog d, const EvalCoef c, const double* __restrict__ bg_sums,
+    const double* __restrict__ tr_sums, int rows_base, int rows_total, int with_grad,
+    double* ell_rows, double* grad_rows, double* blockpart) {
   __shared__ double s_red[6][kFinishThreads];
   const int tid = threadIdx.x;
   const int li = blockIdx.x * kFinishThreads + tid;
   double acc[6] = {0, 0, 0, 0, 0, 0};
   if (li < rows_total) {
     const size_t plane = static_cast<size_t>(rows_total);
-    double B = 0, B2 = 0, T = 0, Td = 0, Tq = 0;
-    for (int s = 0; s < slots; ++s) {
-      const double* p = partial + static_cast<size_t>(s) * 5 * plane + li;
-      B += p[0];
-      B2 += p[plane];
-      T += p[2 * plane];
-      Td += p[3 * plane];
-      Tq += p[4 * plane];
-    }
+    const double B = bg_sums[li], B2 = bg_sums[plane + li];
+    const double T = tr_sums[li], Td = tr_sums[plane + li], Tq = tr_sums[2 * plane + li];
     const double ti = d.t[rows_base + li];
     const double S = c.a * B + c.c * T;
     const double lg = log(fmax(S, kRateClip));  // == combine_lanes, model.hpp:311-326
@@ -611,9 +685,10 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
 }
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
-                 double* partial, int rows_base, int rows_total, bool with_grad, cudaStream_t s) {
+                 double* partial, int rows_base, int rows_total, bool with_grad, int halves,
+                 cudaStream_t s) {
   if (n_items <= 0) return;
-  PairParams P{d, c, items, partial, rows_base, rows_total};
+  PairParams P{d, c, items, partial, rows_base, rows_total, halves};
   const int key = (c.varying ? 6 : 0) + (with_grad ? 3 : 0) + c.mode;
   switch (key) {
     case 0: launch_pair_t<false, false, kExact>(P, n_items, s); break;
@@ -631,11 +706,18 @@ void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, i
   }
 }
 
-int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* partial, int slots,
-                  int rows_base, int rows_total, bool with_grad, double* ell_rows,
-                  double* grad_rows, double* blockpart, cudaStream_t s) {
+void launch_collapse(const double* partial, int slots, int rows_total, double* bg_sums,
+                     double* tr_sums, cudaStream_t s) {
+  const int threads = 256;
+  collapse_kernel<<<(rows_total + threads - 1) / threads, threads, 0, s>>>(partial, slots, rows_total,
+                                                                         bg_sums, tr_sums);
+}
+
+int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* bg_sums,
+                  const double* tr_sums, int rows_base, int rows_total, bool with_grad,
+                  double* ell_rows, double* grad_rows, double* blockpart, cudaStream_t s) {
   const int blocks = (rows_total + kFinishThreads - 1) / kFinishThreads;
-  finish_kernel<<<blocks, kFinishThreads, 0, s>>>(d, c, partial, slots, rows_base, rows_total,
+  finish_kernel<<<blocks, kFinishThreads, 0, s>>>(d, c, bg_sums, tr_sums, rows_base, rows_total,
                                                    with_grad ? 1 : 0, ell_rows, grad_rows,
                                                    blockpart);
   return blocks;

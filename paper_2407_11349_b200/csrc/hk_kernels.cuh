@@ -49,15 +49,22 @@ struct DeviceCatalog {
   double* z;         // prep: q_j w_j                                 [npad]
 };
 
+// Row-sum halves: the background [B, B2] and the trigger [T, Td, Tq].
+constexpr int kHalfBg = 1, kHalfTr = 2;
+
 void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
-                 double* partial, int rows_base, int rows_total, bool with_grad, cudaStream_t s);
-// Combines the partial slots per row, forms ell_n and its gradient, and
-// reduces to one 6-vector per block; writes per-row outputs for rows in
-// [out_b, out_e) when the pointers are non-null.
-int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* partial, int slots,
-                  int rows_base, int rows_total, bool with_grad, double* ell_rows,
-                  double* grad_rows, double* blockpart, cudaStream_t s);
+                 double* partial, int rows_base, int rows_total, bool with_grad, int halves,
+                 cudaStream_t s);
+// Sums the partial slots per row (fixed order) into the background plane
+// pair [B, B2] and/or the trigger planes [T, Td, Tq] (either may be null).
+void launch_collapse(const double* partial, int slots, int rows_total, double* bg_sums,
+                     double* tr_sums, cudaStream_t s);
+// Forms ell_n and its gradient from the row sums and reduces to one
+// 6-vector per block; writes per-row outputs when the pointers are non-null.
+int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* bg_sums,
+                  const double* tr_sums, int rows_base, int rows_total, bool with_grad,
+                  double* ell_rows, double* grad_rows, double* blockpart, cudaStream_t s);
 void launch_reduce(const double* blockpart, int n_blocks, double* out6, cudaStream_t s);
 double measure_fp64_peak(int device, double* ms);
 

@@ -206,6 +206,22 @@ class Evaluator:
                           g.ctypes.data_as(C.c_void_p) if grad else None))
         return (ll.value, g) if grad else ll.value
 
+    def ws_eval(self, params: HawkesParams, grad: bool = False, force: bool = False):
+        """Workspace evaluation (hk_ws_eval): reuses the cached background
+        half while tau_t is unchanged and the trigger half while sigma_x,
+        sigma_t, the variant and the locations are unchanged."""
+        p = params.to_c()
+        ll = C.c_double()
+        g = np.zeros(5)
+        check(lib.hk_ws_eval(self._h, C.byref(p), int(force), C.byref(ll),
+                             g.ctypes.data_as(C.c_void_p) if grad else None))
+        return (ll.value, g) if grad else ll.value
+
+    def ws_stats(self):
+        h, m = C.c_long(), C.c_long()
+        check(lib.hk_ws_stats(self._h, C.byref(h), C.byref(m)))
+        return h.value, m.value
+
     def eval_async(self, params: HawkesParams, grad: bool = True) -> None:
         p = params.to_c()
         check(lib.hk_eval_async(self._h, C.byref(p), int(grad)))
@@ -282,31 +298,30 @@ def event_contribution(p: HawkesParams, catalog: Catalog, n: int) -> float:
 
 
 class LikelihoodWorkspace:
-    """LikelihoodWorkspace<double> (engine.hpp:117-229) on the engine: same
-    methods and semantics (proposal evaluated, promoted on commit), every
-    evaluation a full device pass."""
+    """LikelihoodWorkspace<double> (engine.hpp:117-229) on the engine, with
+    the per-row background [B, B2] and trigger [T, Td, Tq] sums cached on the
+    device: a mu0/xi0 proposal recombines cached sums in O(N), tau_t refreshes
+    only the background, sigma_x/sigma_t (or set_locations) only the trigger.
+    Results are bitwise identical to a fresh evaluation at every setting."""
 
     def __init__(self, catalog: Catalog, variant: Variant, workers: int = 1):
         self._catalog = catalog
         self._variant = Variant(variant)
         self._ev = Evaluator(catalog)
-        self._proposal = None
-        self._current = None
 
-    def evaluate_full(self, p: HawkesParams) -> float:
-        p = replace(p, variant=self._variant)
-        self._current = p
-        return self._ev.eval(p)
+    def evaluate_full(self, p: HawkesParams, grad: bool = False):
+        return self._ev.ws_eval(replace(p, variant=self._variant), grad=grad, force=True)
 
-    def evaluate_proposal(self, p: HawkesParams) -> float:
-        p = replace(p, variant=self._variant)
-        self._proposal = p
-        return self._ev.eval(p)
+    def evaluate_proposal(self, p: HawkesParams, grad: bool = False):
+        return self._ev.ws_eval(replace(p, variant=self._variant), grad=grad)
 
     def commit_proposal(self) -> None:
-        if self._proposal is not None:
-            self._current = self._proposal
-        self._proposal = None
+        """The device cache keeps the current and the proposal state (two
+        entries per half), so promotion needs no work."""
 
     def set_locations(self, lon, lat) -> None:
         self._ev.set_locations(lon, lat)
+
+    def stats(self):
+        """(cache hits, misses) of the workspace evaluations so far."""
+        return self._ev.ws_stats()

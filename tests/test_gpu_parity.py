@@ -328,3 +328,49 @@ def test_full_60k_vs_reference_and_oracle(eng, oracle, reference, variant):
     assert abs(ll - ll_o) <= LL_TOL * abs(ll_o)
     _, scale = oracle.grad_scale(cat.arrays(), p, variant)
     check_grad(g, g_o, scale)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_workspace_cache_bitwise_and_reuse(eng, variant):
+    """Device-cached LikelihoodWorkspace (engine.hpp:117-229 semantics):
+    every cached evaluation is bitwise equal to a fresh one, and only the
+    halves whose parameters changed are recomputed."""
+    cat = eng.benchmark_catalog(50000, 12)
+    ev = eng.Evaluator(cat)
+    base = eng.HawkesParams(**BENCH, variant=eng.Variant(variant))
+    seq = [base,
+           base.with_(mu0=1.7, xi0=0.3),          # recombine only
+           base.with_(mu0=1.7, xi0=0.3, tau_t=7.0),   # background refresh
+           base.with_(mu0=1.7, xi0=0.3),          # back to the cached state
+           base.with_(sigma_x=0.4),               # trigger refresh
+           base.with_(sigma_x=0.4, sigma_t=2.5)]  # trigger refresh
+    fresh = [eng.Evaluator(cat).eval(p, grad=True) for p in seq]
+    h0, m0 = ev.ws_stats()
+    got = [ev.ws_eval(p, grad=True) for p in seq]
+    for (a, ga), (b, gb) in zip(got, fresh):
+        assert a == b and np.array_equal(ga, gb)
+    h1, m1 = ev.ws_stats()
+    assert (h1 - h0, m1 - m0) == (2, 4)  # seq[1] and seq[3] reuse both halves
+    # locations drop the trigger cache only
+    rng = np.random.default_rng(1)
+    lon, lat = rng.uniform(-5, 5, len(cat)), rng.uniform(-5, 5, len(cat))
+    ev.set_locations(lon, lat)
+    a = ev.ws_eval(seq[4], grad=True)
+    b = eng.Evaluator(eng.Catalog(cat.t, lon, lat, cat.density)).eval(seq[4], grad=True)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1])
+
+
+def test_workspace_golden_script_cached(eng):
+    """The reference workspace script (test_engine.cpp:159-190) through the
+    cached workspace."""
+    w = golden("workspace.json")
+    cat = eng.Catalog(*w["catalog"])
+    ws = eng.LikelihoodWorkspace(cat, eng.Variant.constant, 2)
+    for op, p, want in zip(w["ops"], w["params"], w["values"]):
+        p = hp(eng, p, 0)
+        if op == 2:
+            ws.commit_proposal()
+            continue
+        got = ws.evaluate_full(p) if op == 0 else ws.evaluate_proposal(p)
+        assert abs(got - want) <= LL_TOL * abs(want)
+    assert ws.stats()[0] >= 2
