@@ -73,6 +73,7 @@ struct DeviceState {
   int rb = 0, re = 0;  // row shard
   double *t = nullptr, *x = nullptr, *y = nullptr, *q = nullptr;
   double *K = nullptr, *thr = nullptr, *w = nullptr, *v = nullptr, *z = nullptr;
+  float4* fxy = nullptr;
   int *lb = nullptr, *ub = nullptr;
   // work plans per variant (rows per item differ, hk_device.cuh)
   hk::Item* items[2] = {nullptr, nullptr};
@@ -88,7 +89,7 @@ struct DeviceState {
   std::size_t prof_used = 0;
 
   hk::DeviceCatalog catalog(int n, int npad) const {
-    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z};
+    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z, fxy};
   }
 };
 
@@ -99,6 +100,7 @@ struct hk_ctx {
   std::vector<double> t, x, y, d;
   std::vector<int> lb, ub;
   double d2_max = 0.0, q_max = 1.0;
+  double cx = 0.0, cy = 0.0, half_extent = 0.0;
   bool unit_density = false;  // every density == 1: varying == constant exactly
   std::vector<DeviceState> devs;
   bool profiling = false;
@@ -131,6 +133,7 @@ struct hk_ctx {
       for (double* p : {s.t, s.x, s.y, s.q, s.K, s.thr, s.w, s.v, s.z, s.partial, s.blockpart, s.out6,
                         s.bg_sums[0], s.bg_sums[1], s.tr_sums[0], s.tr_sums[1]})
         if (p) cudaFree(p);
+      if (s.fxy) cudaFree(s.fxy);
       if (s.lb) cudaFree(s.lb);
       if (s.ub) cudaFree(s.ub);
       for (hk::Item* it : s.items)
@@ -154,6 +157,9 @@ struct hk_ctx {
     }
     const double w = xmax - xmin, h = ymax - ymin;
     d2_max = w * w + h * h;
+    cx = 0.5 * (xmin + xmax);
+    cy = 0.5 * (ymin + ymax);
+    half_extent = 0.5 * std::max(w, h);
   }
 
   void upload_padded(DeviceState& s, double* dst, const std::vector<double>& src, double pad) {
@@ -179,6 +185,7 @@ struct hk_ctx {
     s.w = dmalloc<double>(npad);
     s.v = dmalloc<double>(npad);
     s.z = dmalloc<double>(npad);
+    s.fxy = dmalloc<float4>(npad);
     s.lb = dmalloc<int>(n);
     s.ub = dmalloc<int>(n);
     upload_padded(s, s.t, t, t[n - 1]);
@@ -228,6 +235,12 @@ struct hk_ctx {
     if (unit_density) in.variant = 0;
     hk::EvalCoef c = hk::make_coef(in, t[0], t[n - 1], d2_max, q_max);
     c.bg_expansion = bg_expansion;
+    c.cx = cx;
+    c.cy = cy;
+    // |fl32(x - cx) - (x - cx)| <= E 2^-24 per coordinate (E = half extent),
+    // twice per difference, plus the FP32 subtraction itself: 8 E 2^-24 bounds
+    // the error of each FP32 coordinate difference with margin.
+    c.f32_err = 8.0 * half_extent * 5.9604644775390625e-08;
     return c;
   }
 

@@ -175,8 +175,8 @@ __device__ __forceinline__ int tile_type_all(int J, const BlockInfo& bi, const P
 }
 
 template <bool kVarying, bool kGrad>
-__device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf, uint64_t* bar,
-                                           const PairParams& P) {
+__device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf, float4* fbuf,
+                                           uint64_t* bar, const PairParams& P) {
   const int j0 = J * kBJ;
   constexpr unsigned kBytes = kBJ * sizeof(double);
   if (type == kTileBx) {  // a group of cnt background-only tiles: their times, contiguous
@@ -193,10 +193,12 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
   } else {  // BT, BTx or T
     mask = (1u << sT) | (1u << sX) | (1u << sY) | (1u << sW);
     if (kGrad) mask |= (1u << sV);
-    if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = thr
+    if (kVarying) mask |= 1u << sK;
     if (kVarying && kGrad) mask |= (1u << sZ);
   }
-  mbar_expect_tx(bar, kBytes * __popc(mask));
+  const bool f32 = kVarying && type != kTileB && type != kTileM;  // FP32 skip-test columns
+  mbar_expect_tx(bar, kBytes * __popc(mask) + (f32 ? kBJ * sizeof(float4) : 0u));
+  if (f32) bulk_g2s(fbuf, P.d.fxy + j0, kBJ * sizeof(float4), bar);
   const double* src[kSlots] = {P.d.t, P.d.x, P.d.y, P.d.w, P.d.v, P.d.z, P.d.K,
                                type == kTileM ? P.d.q : P.d.thr};
 #pragma unroll
@@ -207,6 +209,7 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
 template <int R>
 struct RowState {
   double t[R], x[R], y[R];
+  float xf[R], yf[R];  // FP32 coordinates in the skip-test frame (varying)
   int lb[R], ub[R];
   double B[R], B2[R], T[R], Td[R], Tq[R];
 };
@@ -214,7 +217,7 @@ struct RowState {
 // BT / B / T tiles: no per-pair guards.
 template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr>
 __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restrict__ buf,
-                                          const EvalCoef& c) {
+                                          const float4* __restrict__ fbuf, const EvalCoef& c) {
   const double* __restrict__ st = buf + sT * kBJ;
   const double* __restrict__ sx = buf + sX * kBJ;
   const double* __restrict__ sy = buf + sY * kBJ;
@@ -222,7 +225,6 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
   const double* __restrict__ sv = buf + sV * kBJ;
   const double* __restrict__ sz = buf + sZ * kBJ;
   const double* __restrict__ sk = buf + sK * kBJ;
-  const double* __restrict__ sthr = buf + sAux * kBJ;
   const double Kb = c.Kb, Kq0 = c.Kq0;
   double Tp[NR], Vp[NR], Qp[NR];
 #pragma unroll
@@ -244,29 +246,31 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
     if (kTr) {
       const double xj = sx[j], yj = sy[j], wj = sw[j];
       const double Kj = kVarying ? sk[j] : Kq0;
-      double d2[NR];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const double dx = R.x[r] - xj, dy = R.y[r] - yj;
-        d2[r] = fma(dx, dx, dy * dy);
-      }
       const double vj = kGrad ? sv[j] : 0.0;
       const double zj = kGrad ? (kVarying ? sz[j] : wj) : 0.0;
-      const int thr_hi = kVarying ? __double2hiint(sthr[j]) : 0;
+      bool go[NR];
+      if (kVarying) {
+        // Warp-uniform skip, per row slot (32 rows): an FP32 distance test
+        // against a conservatively rounded-up threshold (prep_kernel) proves
+        // every lane's spatial factor flushes to 0, so skipping is exact.
+        // All slots are tested before any branch so the tests overlap.
+        const float4 fj = fbuf[j];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const float dxf = R.xf[r] - fj.x, dyf = R.yf[r] - fj.y;
+          go[r] = __any_sync(0xffffffffu, fmaf(dxf, dxf, dyf * dyf) <= fj.z);
+        }
+      }
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        if (kVarying) {
-          // Warp-uniform skip, per row slot (32 rows), when every lane's
-          // spatial factor flushes to 0: d^2 above the per-source threshold
-          // (high-word integer compare of non-negative doubles is
-          // order-preserving and conservative), so skipping is exact.
-          if (!__any_sync(0xffffffffu, __double2hiint(d2[r]) <= thr_hi)) continue;
-        }
-        const double e = exp2_16<kMode>(d2[r], Kj);
+        if (kVarying && !go[r]) continue;
+        const double dx = R.x[r] - xj, dy = R.y[r] - yj;
+        const double d2 = fma(dx, dx, dy * dy);
+        const double e = exp2_16<kMode>(d2, Kj);
         Tp[r] = fma(wj, e, Tp[r]);
         if (kGrad) {
           Vp[r] = fma(vj, e, Vp[r]);
-          Qp[r] = fma(zj, d2[r] * e, Qp[r]);
+          Qp[r] = fma(zj, d2 * e, Qp[r]);
         }
       }
     }
@@ -410,6 +414,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     pair_kernel(const PairParams P) {
   constexpr int NR = rows_per_thread(kVarying);
   __shared__ __align__(128) double s_buf[2][kSlots * kBJ];
+  __shared__ __align__(128) float4 s_fbuf[kVarying ? 2 : 1][kVarying ? kBJ : 1];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ double s_red[kThreads / 32][kNM];
 
@@ -440,6 +445,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     R.t[r] = P.d.t[row];
     R.x[r] = P.d.x[row];
     R.y[r] = P.d.y[row];
+    R.xf[r] = __double2float_rn(R.x[r] - P.c.cx);
+    R.yf[r] = __double2float_rn(R.y[r] - P.c.cy);
     R.lb[r] = P.d.lb[row];
     R.ub[r] = P.d.ub[row];
     R.B[r] = R.B2[r] = R.T[r] = R.Td[r] = R.Tq[r] = 0.0;
@@ -469,27 +476,29 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
   int stage = 0;
   unsigned phases = 0u;  // bit s = parity of the next wait on stage s
   if (cur.cnt && tid == 0)
-    issue_tile<kVarying, kGrad>(cur.type, cur.J, cur.cnt, s_buf[0], &s_bar[0], P);
+    issue_tile<kVarying, kGrad>(cur.type, cur.J, cur.cnt, s_buf[0], s_fbuf[0], &s_bar[0], P);
   while (cur.cnt) {
     const Unit nxt = unit_at(cur.J + cur.cnt);
     if (nxt.cnt && tid == 0)
-      issue_tile<kVarying, kGrad>(nxt.type, nxt.J, nxt.cnt, s_buf[stage ^ 1], &s_bar[stage ^ 1], P);
+      issue_tile<kVarying, kGrad>(nxt.type, nxt.J, nxt.cnt, s_buf[stage ^ 1],
+                                  s_fbuf[kVarying ? stage ^ 1 : 0], &s_bar[stage ^ 1], P);
     mbar_wait(&s_bar[stage], (phases >> stage) & 1u);
     phases ^= 1u << stage;
     const double* buf = s_buf[stage];
+    const float4* fbuf = s_fbuf[kVarying ? stage : 0];
     switch (cur.type) {
       case kTileBT:
-        tile_fast<NR, kVarying, kGrad, kMode, true, true>(R, buf, P.c);
+        tile_fast<NR, kVarying, kGrad, kMode, true, true>(R, buf, fbuf, P.c);
         break;
       case kTileB:
-        tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, P.c);
+        tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, fbuf, P.c);
         break;
       case kTileT:
-        tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, P.c);
+        tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, fbuf, P.c);
         break;
       case kTileBTx:
         bg_expansion<NR, kGrad, kMode>(R, buf + sT * kBJ, kBJ, bi, P.c, s_red);
-        tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, P.c);
+        tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, fbuf, P.c);
         break;
       case kTileBx:
         bg_expansion<NR, kGrad, kMode>(R, buf, cur.cnt * kBJ, bi, P.c, s_red);
@@ -534,7 +543,14 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
     d.w[j] = w;
     d.v[j] = dtr * w;
     d.z[j] = q * w;
+    // FP32 skip threshold, rounded up: d2f > thrf implies the exact d^2 > thr
+    // (|d_f - d| <= 2 f32_err), i.e. the pair's spatial factor flushes to 0.
+    const double r = sqrt(kFlushArg / (-K)) + 2.0 * c.f32_err;
+    const float thrf = __double2float_ru(r * r * (1.0 + 1.0 / 262144.0));
+    d.fxy[j] = make_float4(__double2float_rn(d.x[j] - c.cx), __double2float_rn(d.y[j] - c.cy), thrf,
+                           0.f);
   } else {
+    d.fxy[j] = make_float4(0.f, 0.f, -1.f, 0.f);
     d.K[j] = -1.0;
     d.thr[j] = 0.0;
     d.w[j] = 0.0;

@@ -30,6 +30,8 @@ struct EvalCoef {
   double u_scale; // 1 / (tau sqrt 2): background kernel = exp(-(u_i - u_j)^2)
   double two_tau2;// 2 tau^2
   int bg_expansion;  // 1: background by the exact block expansion where it qualifies
+  double cx, cy;  // centre of the locations' bounding box (FP32 skip test frame)
+  double f32_err; // bound on |FP32 distance - exact distance| in that frame
   int varying;
   int mode;       // ExpMode: kExact / kFlush / kChecked from the argument bound
 };
@@ -47,6 +49,7 @@ struct DeviceCatalog {
   double* w;         // prep: q_j exp(-omega (t_ref(J) - t_j))        [npad]
   double* v;         // prep: (t_ref(J) - t_j) w_j                    [npad]
   double* z;         // prep: q_j w_j                                 [npad]
+  float4* fxy;       // prep: {x_j - cx, y_j - cy, thrf_j, 0} in FP32     [npad]
 };
 
 // Row-sum halves: the background [B, B2] and the trigger [T, Td, Tq].
