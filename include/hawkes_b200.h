@@ -97,6 +97,14 @@ int hk_set_locations_device(hk_ctx* ctx, const double* lon_device, const double*
  * receives d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t).  Synchronous. */
 int hk_eval(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5);
 
+/* Precision::single (engine.hpp:106-109 with EvalData<float>): the
+ * trigger pair sums in FP32 (centred FP32 coordinates, MUFU ex2, FP32
+ * partial sums per 256-column tile accumulated in FP64); background and
+ * row epilogue in FP64.  Log-likelihood only, like the reference's single
+ * path.  Agrees with the double result to ~1e-6 relative (the reference's
+ * own single-precision gate is 1e-4, acceptance.cpp:82). */
+int hk_eval_single(hk_ctx* ctx, const hk_params* p, double* ll);
+
 /* Workspace evaluation (LikelihoodWorkspace<double>, engine.hpp:117-229):
  * like hk_eval, but the per-row background sums [B, B2] are reused while
  * tau_t is unchanged and the trigger sums [T, Td, Tq] while sigma_x,

@@ -13,8 +13,8 @@
 // The Partition argument is validated exactly like the reference
 // (engine.hpp:104-105) but the GPU engine shards rows with its own cost
 // model; results agree with the reference within 1e-10 relative (they are
-// bitwise repeatable for a fixed device set).  Precision::single throws
-// std::invalid_argument: the GPU path is FP64 and there is no CPU fallback.
+// bitwise repeatable for a fixed device set).  Precision::single evaluates
+// the trigger sums in FP32 on the GPU (LL only); there is no CPU fallback.
 //
 // See INTEGRATION.md for how a maintainer routes hawkes::log_likelihood and
 // the Sampler's LikelihoodWorkspace here.
@@ -82,6 +82,13 @@ class Engine {
     return ll;
   }
 
+  double log_likelihood_single(const HawkesParams& p, Variant v) const {
+    const hk_params c = detail::to_c(p, v);
+    double ll = 0.0;
+    detail::check(hk_eval_single(ctx_.get(), &c, &ll));
+    return ll;
+  }
+
   double log_likelihood_and_gradient(const HawkesParams& p, Variant v,
                                      std::array<double, 5>& grad) const {
     const hk_params c = detail::to_c(p, v);
@@ -113,27 +120,25 @@ class Engine {
   std::unique_ptr<hk_ctx, void (*)(hk_ctx*)> ctx_;
 };
 
-inline void check_call(const Catalog& catalog, const HawkesParams& p, const Partition& part,
-                       Precision precision) {
+inline void check_call(const Catalog& catalog, const HawkesParams& p, const Partition& part) {
   p.validate();
   if (part.ranges.empty() || part.ranges.back().second != catalog.size())
     throw std::invalid_argument("log_likelihood: partition does not cover the catalog");
-  if (precision != Precision::dbl)
-    throw std::invalid_argument(
-        "log_likelihood: the B200 engine evaluates in double precision only");
 }
 
-/// engine.hpp:101-110 on the GPU.
+/// engine.hpp:101-110 on the GPU (Precision::single: FP32 trigger arithmetic).
 inline double log_likelihood(const Catalog& catalog, const HawkesParams& p, const Partition& part,
                              Precision precision) {
-  check_call(catalog, p, part, precision);
-  return Engine(catalog).log_likelihood(p, p.variant);
+  check_call(catalog, p, part);
+  Engine e(catalog);
+  return precision == Precision::dbl ? e.log_likelihood(p, p.variant)
+                                     : e.log_likelihood_single(p, p.variant);
 }
 
 /// The log-likelihood and d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t).
 inline double log_likelihood_and_gradient(const Catalog& catalog, const HawkesParams& p,
                                           const Partition& part, std::array<double, 5>& grad) {
-  check_call(catalog, p, part, Precision::dbl);
+  check_call(catalog, p, part);
   return Engine(catalog).log_likelihood_and_gradient(p, p.variant, grad);
 }
 
@@ -151,28 +156,24 @@ inline double event_contribution(const HawkesParams& p, const Catalog& catalog, 
 /// only the trigger; results are bitwise identical to a full evaluation.
 template <typename Real>
 class LikelihoodWorkspace {
-  // Precision::single (Real = float) is rejected at construction, like
-  // log_likelihood: there is no single-precision GPU path yet and no CPU
-  // fallback.
-  static const Catalog& require_double(const Catalog& catalog) {
-    if (!std::is_same_v<Real, double>)
-      throw std::invalid_argument(
-          "LikelihoodWorkspace: the B200 engine evaluates in double precision only");
-    return catalog;
-  }
+  static constexpr bool kDouble = std::is_same_v<Real, double>;
 
  public:
   LikelihoodWorkspace(const Catalog& catalog, Variant variant, std::size_t /*workers*/)
-      : engine_(require_double(catalog)), variant_(variant) {}
+      : engine_(catalog), variant_(variant) {}
 
+  // Real = float (Precision::single) evaluates through the FP32 trigger path
+  // without caching; Real = double uses the device-cached row sums.
   double evaluate_full(const HawkesParams& p) {
     current_ = p;
-    return engine_.workspace_eval(p, variant_, /*force=*/true);
+    return kDouble ? engine_.workspace_eval(p, variant_, /*force=*/true)
+                   : engine_.log_likelihood_single(p, variant_);
   }
 
   double evaluate_proposal(const HawkesParams& p) {
     proposal_ = p;
-    return engine_.workspace_eval(p, variant_, /*force=*/false);
+    return kDouble ? engine_.workspace_eval(p, variant_, /*force=*/false)
+                   : engine_.log_likelihood_single(p, variant_);
   }
 
   // Both the current and the proposal state stay cached on the device.

@@ -48,6 +48,7 @@ SIGNATURES = [
     ("hk_set_locations", C.c_int, [_ctx, _dp, _dp]),
     ("hk_set_locations_device", C.c_int, [_ctx, C.c_void_p, C.c_void_p]),
     ("hk_eval", C.c_int, [_ctx, _pp, C.POINTER(C.c_double), C.c_void_p]),
+    ("hk_eval_single", C.c_int, [_ctx, _pp, C.POINTER(C.c_double)]),
     ("hk_ws_eval", C.c_int, [_ctx, _pp, C.c_int, C.POINTER(C.c_double), C.c_void_p]),
     ("hk_ws_stats", C.c_int, [_ctx, C.POINTER(C.c_long), C.POINTER(C.c_long)]),
     ("hk_eval_async", C.c_int, [_ctx, _pp, C.c_int]),

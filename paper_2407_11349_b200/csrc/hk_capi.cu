@@ -74,6 +74,7 @@ struct DeviceState {
   double *t = nullptr, *x = nullptr, *y = nullptr, *q = nullptr;
   double *K = nullptr, *thr = nullptr, *w = nullptr, *v = nullptr, *z = nullptr;
   float4* fxy = nullptr;
+  float2* fkw = nullptr;
   int *lb = nullptr, *ub = nullptr;
   // work plans per variant (rows per item differ, hk_device.cuh)
   hk::Item* items[2] = {nullptr, nullptr};
@@ -89,7 +90,7 @@ struct DeviceState {
   std::size_t prof_used = 0;
 
   hk::DeviceCatalog catalog(int n, int npad) const {
-    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z, fxy};
+    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z, fxy, fkw};
   }
 };
 
@@ -134,6 +135,7 @@ struct hk_ctx {
                         s.bg_sums[0], s.bg_sums[1], s.tr_sums[0], s.tr_sums[1]})
         if (p) cudaFree(p);
       if (s.fxy) cudaFree(s.fxy);
+      if (s.fkw) cudaFree(s.fkw);
       if (s.lb) cudaFree(s.lb);
       if (s.ub) cudaFree(s.ub);
       for (hk::Item* it : s.items)
@@ -186,6 +188,7 @@ struct hk_ctx {
     s.v = dmalloc<double>(npad);
     s.z = dmalloc<double>(npad);
     s.fxy = dmalloc<float4>(npad);
+    s.fkw = dmalloc<float2>(npad);
     s.lb = dmalloc<int>(n);
     s.ub = dmalloc<int>(n);
     upload_padded(s, s.t, t, t[n - 1]);
@@ -225,7 +228,7 @@ struct hk_ctx {
     return s.prof_events[s.prof_used++];
   }
 
-  hk::EvalCoef coef(const hk_params* p) const {
+  hk::EvalCoef coef(const hk_params* p, bool single = false) const {
     if (!p) throw std::invalid_argument("hk_eval: null params");
     hk::ParamsIn in{p->mu0, p->tau_t, p->xi0, p->sigma_x, p->sigma_t, p->area, p->variant};
     hk::validate_params(in);
@@ -241,8 +244,12 @@ struct hk_ctx {
     // twice per difference, plus the FP32 subtraction itself: 8 E 2^-24 bounds
     // the error of each FP32 coordinate difference with margin.
     c.f32_err = 8.0 * half_extent * 5.9604644775390625e-08;
+    c.single_prec = single ? 1 : 0;
     return c;
   }
+
+  // The trigger half depends on the variant and on the precision.
+  static int tr_variant(const hk::EvalCoef& c) { return c.varying + 2 * c.single_prec; }
 
   // Picks the cache entry for each half: a hit (unless forced) or the least
   // recently used entry, which the next enqueue recomputes.  Returns the
@@ -252,7 +259,7 @@ struct hk_ctx {
       return k.valid && k.a == c.tau_t && k.bgx == c.bg_expansion && (k.grad || !grad);
     };
     auto hit_tr = [&](const Key& k) {
-      return k.valid && k.a == c.sigma_x && k.b == c.sigma_t && k.variant == c.varying &&
+      return k.valid && k.a == c.sigma_x && k.b == c.sigma_t && k.variant == tr_variant(c) &&
              k.loc == loc_version && (k.grad || !grad);
     };
     int halves = 0;
@@ -271,7 +278,7 @@ struct hk_ctx {
     if (tri < 0) {
       halves |= hk::kHalfTr;
       tri = tr_key[0].used <= tr_key[1].used ? 0 : 1;
-      tr_key[tri] = Key{true, c.sigma_x, c.sigma_t, c.varying, grad ? 1 : 0, 0, loc_version, 0};
+      tr_key[tri] = Key{true, c.sigma_x, c.sigma_t, tr_variant(c), grad ? 1 : 0, 0, loc_version, 0};
     }
     bg_key[bgi].used = ++clock;
     tr_key[tri].used = ++clock;
@@ -307,8 +314,9 @@ struct hk_ctx {
   }
 
   // Full or workspace evaluation on every device; sums in device order.
-  void evaluate(const hk_params* p, bool grad, bool workspace, bool force, double* ll, double* grad5) {
-    const hk::EvalCoef c = coef(p);
+  void evaluate(const hk_params* p, bool grad, bool workspace, bool force, double* ll, double* grad5,
+                bool single = false) {
+    const hk::EvalCoef c = coef(p, single);
     int bgi, tri;
     const int halves = workspace ? plan_halves(c, grad, force, bgi, tri)
                                  : plan_halves(c, grad, /*force=*/true, bgi, tri);
@@ -446,6 +454,13 @@ int hk_eval(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5) {
   return guarded([&] {
     if (!ctx || !ll) throw std::invalid_argument("hk_eval: null argument");
     ctx->evaluate(p, grad5 != nullptr, /*workspace=*/false, /*force=*/true, ll, grad5);
+  });
+}
+
+int hk_eval_single(hk_ctx* ctx, const hk_params* p, double* ll) {
+  return guarded([&] {
+    if (!ctx || !ll) throw std::invalid_argument("hk_eval_single: null argument");
+    ctx->evaluate(p, /*grad=*/false, /*workspace=*/false, /*force=*/true, ll, nullptr, /*single=*/true);
   });
 }
 

@@ -174,9 +174,9 @@ __device__ __forceinline__ int tile_type_all(int J, const BlockInfo& bi, const P
   return kTileM;
 }
 
-template <bool kVarying, bool kGrad>
+template <bool kVarying, bool kGrad, bool kF32>
 __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf, float4* fbuf,
-                                           uint64_t* bar, const PairParams& P) {
+                                           float2* kwbuf, uint64_t* bar, const PairParams& P) {
   const int j0 = J * kBJ;
   constexpr unsigned kBytes = kBJ * sizeof(double);
   if (type == kTileBx) {  // a group of cnt background-only tiles: their times, contiguous
@@ -185,6 +185,15 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
     return;
   }
   unsigned mask = 0;
+  if (kF32 && (type == kTileBT || type == kTileBTx || type == kTileT)) {
+    // single precision: times (FP64 background / row factors) + the FP32
+    // trigger columns {x, y, thr} and {K, w}
+    mbar_expect_tx(bar, kBytes + kBJ * (sizeof(float4) + sizeof(float2)));
+    bulk_g2s(buf + sT * kBJ, P.d.t + j0, kBytes, bar);
+    bulk_g2s(fbuf, P.d.fxy + j0, kBJ * sizeof(float4), bar);
+    bulk_g2s(kwbuf, P.d.fkw + j0, kBJ * sizeof(float2), bar);
+    return;
+  }
   if (type == kTileB) {
     mask = 1u << sT;
   } else if (type == kTileM) {
@@ -287,6 +296,43 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
         R.Tq[r] = fma(E, Qp[r], R.Tq[r]);
       }
     }
+  }
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));  // MUFU.EX2, subnormals kept
+  return y;
+}
+
+// Precision::single trigger of a BT/BTx/T tile (the reference's float path,
+// model.hpp:183-208 / :271-296, evaluated with MUFU ex2): FP32 distances in
+// the centred frame, FP32 partial sums within the tile, then the FP64 row
+// factor exp(-omega (t_i - t_ref)) and an FP64 accumulator across tiles.
+template <int NR, bool kVarying, int kMode>
+__device__ __forceinline__ void tile_trig_f32(RowState<NR>& R, const double* __restrict__ st,
+                                              const float4* __restrict__ fbuf,
+                                              const float2* __restrict__ kwbuf, const EvalCoef& c) {
+  float Tp[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) Tp[r] = 0.f;
+#pragma unroll 4
+  for (int j = 0; j < kBJ; ++j) {
+    const float4 fj = fbuf[j];
+    const float2 kw = kwbuf[j];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const float dx = R.xf[r] - fj.x, dy = R.yf[r] - fj.y;
+      const float d2 = fmaf(dx, dx, dy * dy);
+      if (kVarying && !__any_sync(0xffffffffu, d2 <= fj.z)) continue;
+      Tp[r] = fmaf(kw.y, ex2_approx(d2 * kw.x), Tp[r]);
+    }
+  }
+  const double t_ref = st[kBJ - 1];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const double E = exp2_16<kMode>(R.t[r] - t_ref, c.Kw);
+    R.T[r] = fma(E, static_cast<double>(Tp[r]), R.T[r]);
   }
 }
 
@@ -409,12 +455,14 @@ __device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
   }
 }
 
-template <bool kVarying, bool kGrad, int kMode>
+template <bool kVarying, bool kGrad, int kMode, bool kF32>
 __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)))
     pair_kernel(const PairParams P) {
   constexpr int NR = rows_per_thread(kVarying);
   __shared__ __align__(128) double s_buf[2][kSlots * kBJ];
-  __shared__ __align__(128) float4 s_fbuf[kVarying ? 2 : 1][kVarying ? kBJ : 1];
+  constexpr bool kUseF = kVarying || kF32;  // FP32 column data staged
+  __shared__ __align__(128) float4 s_fbuf[kUseF ? 2 : 1][kUseF ? kBJ : 1];
+  __shared__ __align__(128) float2 s_kwbuf[kF32 ? 2 : 1][kF32 ? kBJ : 1];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ double s_red[kThreads / 32][kNM];
 
@@ -476,17 +524,24 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
   int stage = 0;
   unsigned phases = 0u;  // bit s = parity of the next wait on stage s
   if (cur.cnt && tid == 0)
-    issue_tile<kVarying, kGrad>(cur.type, cur.J, cur.cnt, s_buf[0], s_fbuf[0], &s_bar[0], P);
+    issue_tile<kVarying, kGrad, kF32>(cur.type, cur.J, cur.cnt, s_buf[0], s_fbuf[0], s_kwbuf[0],
+                                      &s_bar[0], P);
   while (cur.cnt) {
     const Unit nxt = unit_at(cur.J + cur.cnt);
     if (nxt.cnt && tid == 0)
-      issue_tile<kVarying, kGrad>(nxt.type, nxt.J, nxt.cnt, s_buf[stage ^ 1],
-                                  s_fbuf[kVarying ? stage ^ 1 : 0], &s_bar[stage ^ 1], P);
+      issue_tile<kVarying, kGrad, kF32>(nxt.type, nxt.J, nxt.cnt, s_buf[stage ^ 1],
+                                        s_fbuf[kUseF ? stage ^ 1 : 0], s_kwbuf[kF32 ? stage ^ 1 : 0],
+                                        &s_bar[stage ^ 1], P);
     mbar_wait(&s_bar[stage], (phases >> stage) & 1u);
     phases ^= 1u << stage;
     const double* buf = s_buf[stage];
-    const float4* fbuf = s_fbuf[kVarying ? stage : 0];
-    switch (cur.type) {
+    const float4* fbuf = s_fbuf[kUseF ? stage : 0];
+    const float2* kwbuf = s_kwbuf[kF32 ? stage : 0];
+    if (kF32 && (cur.type == kTileBT || cur.type == kTileBTx || cur.type == kTileT)) {
+      if (cur.type == kTileBT) tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, fbuf, P.c);
+      if (cur.type == kTileBTx) bg_expansion<NR, kGrad, kMode>(R, buf + sT * kBJ, kBJ, bi, P.c, s_red);
+      tile_trig_f32<NR, kVarying, kMode>(R, buf + sT * kBJ, fbuf, kwbuf, P.c);
+    } else switch (cur.type) {
       case kTileBT:
         tile_fast<NR, kVarying, kGrad, kMode, true, true>(R, buf, fbuf, P.c);
         break;
@@ -549,8 +604,11 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
     const float thrf = __double2float_ru(r * r * (1.0 + 1.0 / 262144.0));
     d.fxy[j] = make_float4(__double2float_rn(d.x[j] - c.cx), __double2float_rn(d.y[j] - c.cy), thrf,
                            0.f);
+    d.fkw[j] = make_float2(__double2float_rn(-(c.half_s2 * q) * 1.4426950408889634),
+                           __double2float_rn(w));
   } else {
     d.fxy[j] = make_float4(0.f, 0.f, -1.f, 0.f);
+    d.fkw[j] = make_float2(0.f, 0.f);
     d.K[j] = -1.0;
     d.thr[j] = 0.0;
     d.w[j] = 0.0;
@@ -688,9 +746,9 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* sink, int iters
   if (r == 12345.678) sink[threadIdx.x] = r;
 }
 
-template <bool V, bool G, int M>
+template <bool V, bool G, int M, bool F>
 void launch_pair_t(const PairParams& P, int n_items, cudaStream_t s) {
-  pair_kernel<V, G, M><<<n_items, kThreads, 0, s>>>(P);
+  pair_kernel<V, G, M, F><<<n_items, kThreads, 0, s>>>(P);
 }
 
 }  // namespace
@@ -705,20 +763,32 @@ void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, i
                  cudaStream_t s) {
   if (n_items <= 0) return;
   PairParams P{d, c, items, partial, rows_base, rows_total, halves};
+  if (c.single_prec) {  // Precision::single: LL only
+    const int key = (c.varying ? 3 : 0) + c.mode;
+    switch (key) {
+      case 0: launch_pair_t<false, false, kExact, true>(P, n_items, s); break;
+      case 1: launch_pair_t<false, false, kFlush, true>(P, n_items, s); break;
+      case 2: launch_pair_t<false, false, kChecked, true>(P, n_items, s); break;
+      case 3: launch_pair_t<true, false, kExact, true>(P, n_items, s); break;
+      case 4: launch_pair_t<true, false, kFlush, true>(P, n_items, s); break;
+      default: launch_pair_t<true, false, kChecked, true>(P, n_items, s); break;
+    }
+    return;
+  }
   const int key = (c.varying ? 6 : 0) + (with_grad ? 3 : 0) + c.mode;
   switch (key) {
-    case 0: launch_pair_t<false, false, kExact>(P, n_items, s); break;
-    case 1: launch_pair_t<false, false, kFlush>(P, n_items, s); break;
-    case 2: launch_pair_t<false, false, kChecked>(P, n_items, s); break;
-    case 3: launch_pair_t<false, true, kExact>(P, n_items, s); break;
-    case 4: launch_pair_t<false, true, kFlush>(P, n_items, s); break;
-    case 5: launch_pair_t<false, true, kChecked>(P, n_items, s); break;
-    case 6: launch_pair_t<true, false, kExact>(P, n_items, s); break;
-    case 7: launch_pair_t<true, false, kFlush>(P, n_items, s); break;
-    case 8: launch_pair_t<true, false, kChecked>(P, n_items, s); break;
-    case 9: launch_pair_t<true, true, kExact>(P, n_items, s); break;
-    case 10: launch_pair_t<true, true, kFlush>(P, n_items, s); break;
-    default: launch_pair_t<true, true, kChecked>(P, n_items, s); break;
+    case 0: launch_pair_t<false, false, kExact, false>(P, n_items, s); break;
+    case 1: launch_pair_t<false, false, kFlush, false>(P, n_items, s); break;
+    case 2: launch_pair_t<false, false, kChecked, false>(P, n_items, s); break;
+    case 3: launch_pair_t<false, true, kExact, false>(P, n_items, s); break;
+    case 4: launch_pair_t<false, true, kFlush, false>(P, n_items, s); break;
+    case 5: launch_pair_t<false, true, kChecked, false>(P, n_items, s); break;
+    case 6: launch_pair_t<true, false, kExact, false>(P, n_items, s); break;
+    case 7: launch_pair_t<true, false, kFlush, false>(P, n_items, s); break;
+    case 8: launch_pair_t<true, false, kChecked, false>(P, n_items, s); break;
+    case 9: launch_pair_t<true, true, kExact, false>(P, n_items, s); break;
+    case 10: launch_pair_t<true, true, kFlush, false>(P, n_items, s); break;
+    default: launch_pair_t<true, true, kChecked, false>(P, n_items, s); break;
   }
 }
 

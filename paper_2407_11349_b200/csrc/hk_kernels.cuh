@@ -32,6 +32,7 @@ struct EvalCoef {
   int bg_expansion;  // 1: background by the exact block expansion where it qualifies
   double cx, cy;  // centre of the locations' bounding box (FP32 skip test frame)
   double f32_err; // bound on |FP32 distance - exact distance| in that frame
+  int single_prec;   // Precision::single: FP32 trigger arithmetic, LL only
   int varying;
   int mode;       // ExpMode: kExact / kFlush / kChecked from the argument bound
 };
@@ -50,6 +51,7 @@ struct DeviceCatalog {
   double* v;         // prep: (t_ref(J) - t_j) w_j                    [npad]
   double* z;         // prep: q_j w_j                                 [npad]
   float4* fxy;       // prep: {x_j - cx, y_j - cy, thrf_j, 0} in FP32     [npad]
+  float2* fkw;       // prep: {K_j log2(e)/(ln2-units), w_j} in FP32 (single precision) [npad]
 };
 
 // Row-sum halves: the background [B, B2] and the trigger [T, Td, Tq].

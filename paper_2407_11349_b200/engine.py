@@ -17,8 +17,8 @@ Names, argument meaning and error behaviour follow the reference:
   (new)                                          log_likelihood_and_gradient
 
 std::invalid_argument maps to ValueError, std::out_of_range to IndexError.
-Precision.single is rejected with ValueError: the GPU path is FP64 and there
-is no CPU fallback.
+Precision.single runs the trigger pair sums in FP32 on the GPU (log-likelihood
+only, like the reference); there is no CPU fallback.
 """
 from __future__ import annotations
 
@@ -206,6 +206,13 @@ class Evaluator:
                           g.ctypes.data_as(C.c_void_p) if grad else None))
         return (ll.value, g) if grad else ll.value
 
+    def eval_single(self, params: HawkesParams) -> float:
+        """Precision.single: FP32 trigger arithmetic, log-likelihood only."""
+        p = params.to_c()
+        ll = C.c_double()
+        check(lib.hk_eval_single(self._h, C.byref(p), C.byref(ll)))
+        return ll.value
+
     def ws_eval(self, params: HawkesParams, grad: bool = False, force: bool = False):
         """Workspace evaluation (hk_ws_eval): reuses the cached background
         half while tau_t is unchanged and the trigger half while sigma_x,
@@ -266,26 +273,28 @@ def _evaluator_for(catalog: Catalog) -> Evaluator:
     return catalog._ctx
 
 
-def _check_call(catalog: Catalog, p: HawkesParams, part: Partition, precision: Precision):
+def _check_call(catalog: Catalog, p: HawkesParams, part: Partition):
     p.validate()
     if not part.ranges or part.ranges[-1][1] != catalog.size():
         raise ValueError("log_likelihood: partition does not cover the catalog")
-    if precision != Precision.dbl:
-        raise ValueError("log_likelihood: the B200 engine evaluates in double precision only "
-                         "(Precision::single is not implemented on the GPU path)")
 
 
 def log_likelihood(catalog: Catalog, p: HawkesParams, part: Partition,
                    precision: Precision = Precision.dbl) -> float:
-    """engine.hpp:101-110 on the B200 engine."""
-    _check_call(catalog, p, part, precision)
-    return _evaluator_for(catalog).eval(p)
+    """engine.hpp:101-110 on the B200 engine (Precision.single: FP32 trigger
+    arithmetic, like the reference's EvalData<float> path)."""
+    _check_call(catalog, p, part)
+    ev = _evaluator_for(catalog)
+    return ev.eval(p) if precision == Precision.dbl else ev.eval_single(p)
 
 
 def log_likelihood_and_gradient(catalog: Catalog, p: HawkesParams, part: Partition | None = None,
                                 precision: Precision = Precision.dbl):
-    """(log-likelihood, d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t))."""
-    _check_call(catalog, p, part or Partition.make(catalog.size(), 1), precision)
+    """(log-likelihood, d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t)); the
+    gradient is evaluated in double precision only."""
+    _check_call(catalog, p, part or Partition.make(catalog.size(), 1))
+    if precision != Precision.dbl:
+        raise ValueError("log_likelihood_and_gradient: the gradient is evaluated in double precision only")
     return _evaluator_for(catalog).eval(p, grad=True)
 
 

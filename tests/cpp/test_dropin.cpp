@@ -75,7 +75,7 @@ void criterion_1_subset() {  // acceptance.cpp:50-84, 20 of its 100 catalogs
   std::uniform_int_distribution<std::size_t> un(10, 5000);
   std::uniform_real_distribution<double> umu(0.1, 2.0), utau(0.5, 20.0), uxi(0.05, 0.9), usx(0.02, 0.5),
       ust(0.2, 10.0);
-  double worst = 0.0;
+  double worst = 0.0, worst_sgl = 0.0;
   for (int c = 0; c < 20; ++c) {
     const std::size_t n = un(rng);
     std::vector<Event> events = benchmark_catalog(n, 9000 + static_cast<std::uint64_t>(c)).events();
@@ -96,12 +96,16 @@ void criterion_1_subset() {  // acceptance.cpp:50-84, 20 of its 100 catalogs
     const double reference = naive_log_likelihood(catalog, p);
     for (std::size_t g : {1, 2, 4, 8}) {
       const double d = b200::log_likelihood(catalog, p, make_partition(n, g), Precision::dbl);
+      const double s = b200::log_likelihood(catalog, p, make_partition(n, g), Precision::single);
       worst = std::max(worst, std::abs(d - reference) / std::abs(reference));
+      worst_sgl = std::max(worst_sgl, std::abs(s - reference) / std::abs(reference));
     }
   }
-  char d[96];
-  std::snprintf(d, sizeof d, "max rel err %.3g (tol 1e-10)", worst);
-  report("criterion 1 catalogs vs naive_log_likelihood (acceptance.cpp:50-84)", worst <= 1e-10, d);
+  char d[128];
+  std::snprintf(d, sizeof d, "max rel err double %.3g (tol 1e-10), single %.3g (tol 1e-4)", worst,
+                worst_sgl);
+  report("criterion 1 catalogs vs naive_log_likelihood (acceptance.cpp:50-84)",
+         worst <= 1e-10 && worst_sgl <= 1e-4, d);
 }
 
 void contributions_and_errors() {
@@ -143,6 +147,35 @@ void contributions_and_errors() {
   }
   report("exception types and messages (types.hpp:92-103, engine.hpp:104-105, model.hpp:352)",
          ok && ok2 && ok3, "invalid_argument / out_of_range");
+}
+
+void criterion_2_single_finite() {  // acceptance.cpp:86-113
+  const std::size_t n = 100000;
+  std::vector<Event> coincident, separated;
+  for (std::size_t i = 0; i < n; ++i) {
+    coincident.push_back({0.0, 0.0, 0.0, "", 1.0});
+    const double corner = i % 2 == 0 ? -180.0 : 180.0;
+    separated.push_back({static_cast<double>(i) * 0.1, corner, corner / 2.0, "", 1.0});
+  }
+  bool ok = true;
+  std::mt19937_64 rng(202);
+  std::uniform_real_distribution<double> umu(0.1, 2.0), utau(0.5, 20.0), uxi(0.05, 0.9), usx(0.02, 0.5),
+      ust(0.2, 10.0);
+  for (const auto& events : {coincident, separated}) {
+    const Catalog catalog(events);
+    for (int rep = 0; rep < 3; ++rep) {
+      HawkesParams p;
+      p.mu0 = umu(rng);
+      p.tau_t = utau(rng);
+      p.xi0 = uxi(rng);
+      p.sigma_x = usx(rng);
+      p.sigma_t = ust(rng);
+      p.area = std::max(domain_area(catalog), 1e-6);
+      ok = ok && std::isfinite(b200::log_likelihood(catalog, p, make_partition(n, 4), Precision::single));
+    }
+  }
+  report("criterion 2: single precision finite on adversarial 100k catalogs (acceptance.cpp:86-113)", ok,
+         ok ? "all evaluations finite" : "non-finite value produced");
 }
 
 void gradient_vs_fd() {
@@ -234,6 +267,7 @@ int main() {
   engine_agrees_with_naive();
   criterion_1_subset();
   contributions_and_errors();
+  criterion_2_single_finite();
   gradient_vs_fd();
   sampler_unchanged();
   std::printf("%d failure(s)\n", failures);

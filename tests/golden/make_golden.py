@@ -106,6 +106,7 @@ def acceptance1(count=24):
             "n": n, "seed": 9000 + c, "float_round": True, "variant": variant, "params": p,
             "sha256": digest(cat),
             "ll": {str(g): R.log_likelihood(cat, p, variant, g) for g in (1, 2, 4, 8)},
+            "ll_single": R.log_likelihood(cat, p, variant, 1, single=True),
             "naive": R.naive_log_likelihood(cat, p, variant),
         })
         print(f"acceptance1 case {c}: n={n}", flush=True)

@@ -219,7 +219,7 @@ def test_errors(eng):
     with pytest.raises(ValueError, match="partition does not cover"):
         eng.log_likelihood(cat, eng.HawkesParams(), eng.Partition.make(99, 2))
     with pytest.raises(ValueError, match="double precision only"):
-        eng.log_likelihood(cat, eng.HawkesParams(), eng.Partition.make(100, 2), eng.Precision.single)
+        eng.log_likelihood_and_gradient(cat, eng.HawkesParams(), None, eng.Precision.single)
 
 
 def test_adversarial_finite(eng, oracle):
@@ -374,3 +374,45 @@ def test_workspace_golden_script_cached(eng):
         got = ws.evaluate_full(p) if op == 0 else ws.evaluate_proposal(p)
         assert abs(got - want) <= LL_TOL * abs(want)
     assert ws.stats()[0] >= 2
+
+
+# ---- Precision::single ----------------------------------
+
+@pytest.mark.parametrize("case", golden("acceptance1.json"), ids=lambda c: f"n{c['n']}v{c['variant']}")
+def test_single_precision_acceptance1(eng, case):
+    """acceptance.cpp:50-84 single-precision gate: within 1e-4 of the naive
+    double evaluator, and close to the reference's own float path."""
+    cat = golden_catalog(case)
+    ll = eng.log_likelihood(eng.Catalog(*cat), hp(eng, case["params"], case["variant"]),
+                            eng.Partition.make(case["n"], 1), eng.Precision.single)
+    assert abs(ll - case["naive"]) <= 1e-4 * abs(case["naive"])
+    assert abs(ll - case["ll_single"]) <= 1e-4 * abs(case["naive"])
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_single_precision_large(eng, variant):
+    """N=2e5 benchmark catalog: single vs double precision engine, 1e-5."""
+    cat = eng.benchmark_catalog(200000, 9)
+    ev = eng.Evaluator(cat)
+    p = hp(eng, BENCH, variant)
+    d = ev.eval(p)
+    f = ev.eval_single(p)
+    assert abs(f - d) <= 1e-5 * abs(d)
+    assert ev.eval_single(p) == f  # deterministic
+
+
+def test_single_precision_adversarial_finite(eng):
+    """acceptance.cpp:86-113 (criterion 2): 100k fully coincident and maximally
+    separated catalogs stay finite in single precision."""
+    n = 100000
+    i = np.arange(n)
+    coincident = eng.Catalog(np.zeros(n), np.zeros(n), np.zeros(n))
+    corner = np.where(i % 2 == 0, -180.0, 180.0)
+    separated = eng.Catalog(i * 0.1, corner, corner / 2.0)
+    rng = np.random.default_rng(202)
+    for cat in (coincident, separated):
+        ev = eng.Evaluator(cat)
+        for _ in range(3):
+            p = eng.HawkesParams(mu0=rng.uniform(0.1, 2), tau_t=rng.uniform(0.5, 20), xi0=rng.uniform(0.05, 0.9),
+                                 sigma_x=rng.uniform(0.02, 0.5), sigma_t=rng.uniform(0.2, 10), area=1.0)
+            assert np.isfinite(ev.eval_single(p))
