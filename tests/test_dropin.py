@@ -18,3 +18,15 @@ def test_cpp_dropin_gate(cuda_device):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failure(s)" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_hmc_gate(cuda_device):
+    """HMC cut-posterior driver (include/hawkes_b200/hmc.hpp) vs the
+    reference's own MH sampler and diagnostics (tests/cpp/test_hmc.cpp)."""
+    b = BIN.parent / "test_hmc"
+    if not b.exists():
+        pytest.skip("oracle/_ref/test_hmc not built (needs /root/reference at build time)")
+    r = subprocess.run([str(b)], capture_output=True, text=True, timeout=1800)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr

@@ -8,6 +8,8 @@ python -m pytest tests -q -m gpu > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/bench.err
 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err
+[ -x build/cut_posterior_bench ] && ./build/cut_posterior_bench 1000000 3 8 1 > $O/config5.json 2> $O/config5.err
+python tools/ws_sweep.py 1000000 1 > $O/ws_sweep.log 2>&1
 if [ "${NCU:-1}" = 1 ]; then
   python bench.py --steps 2 --warmup 1 > $O/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
