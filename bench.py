@@ -254,6 +254,30 @@ def run_ours(args):
     if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total, pair_ms_avg = float(t[0]), float(t[1])
+
+    # ---- the same step on the direct per-pair path (background expansion
+    # off): the pure O(N^2) kernel, for the FP64-pipe roofline of SURVEY 8(d)
+    direct_steps = 2
+    ev.set_bg_expansion(False)
+    step()
+    torch.cuda.synchronize()
+    ev.reset_profile()
+    ev.set_profiling(True)
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        d0.record()
+    for _ in range(direct_steps):
+        step()
+    with torch.cuda.stream(stream):
+        d1.record()
+    torch.cuda.synchronize()
+    dpair_ms, dpair_n, _ = ev.profile()
+    ev.set_profiling(False)
+    ev.set_bg_expansion(True)
+    t = torch.tensor([d0.elapsed_time(d1), dpair_ms / max(dpair_n, 1)], dtype=torch.float64, device=dev)
+    if use_dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    direct_ms_total, direct_pair_ms = float(t[0]), float(t[1])
     # result of the last step, for the record
     if sh is not None:
         ll, g = sh.eval(p, grad=True)
@@ -339,6 +363,14 @@ def run_ours(args):
                                        "than the convention (exact background block expansion + 64-entry-table "
                                        "exp); the pipe's real utilisation is `ncu.fp64_pipe_active`",
                          "ncu": ncu},
+            "direct_kernel": {
+                "note": "the same LL+grad step with the background block expansion disabled "
+                        "(HK_OPT_BG_EXPANSION=0): every ordered pair evaluated directly",
+                "value": direct_steps / (direct_ms_total * 1e-3), "unit": "evals/s",
+                "ms_per_step": direct_ms_total / direct_steps,
+                "roofline": {"bound": "fp64", "achieved": pairs_local * FP64_PER_PAIR * 2 / (direct_pair_ms * 1e-3) / 1e12,
+                             "peak": fp64_peak, "unit": "TFLOP/s",
+                             "frac": pairs_local * FP64_PER_PAIR * 2 / (direct_pair_ms * 1e-3) / 1e12 / fp64_peak}},
             "cpu_baseline": cpu,
             "clocks": clk,
             "result": {"loglik": ll, "grad": [float(x) for x in g]},
