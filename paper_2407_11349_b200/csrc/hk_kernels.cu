@@ -239,6 +239,7 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
 #pragma unroll
   for (int r = 0; r < NR; ++r) Tp[r] = Vp[r] = Qp[r] = 0.0;
 
+  constexpr bool kTrDense = kTr && !kVarying;  // every pair computed
 #pragma unroll kUnroll
   for (int j = 0; j < kBJ; ++j) {
     if (kBg) {
@@ -252,34 +253,58 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
         if (kGrad) R.B2[r] = fma(td2, b, R.B2[r]);
       }
     }
-    if (kTr) {
+    if (kTrDense) {
       const double xj = sx[j], yj = sy[j], wj = sw[j];
-      const double Kj = kVarying ? sk[j] : Kq0;
       const double vj = kGrad ? sv[j] : 0.0;
-      const double zj = kGrad ? (kVarying ? sz[j] : wj) : 0.0;
-      bool go[NR];
-      if (kVarying) {
-        // Warp-uniform skip, per row slot (32 rows): an FP32 distance test
-        // against a conservatively rounded-up threshold (prep_kernel) proves
-        // every lane's spatial factor flushes to 0, so skipping is exact.
-        // All slots are tested before any branch so the tests overlap.
-        const float4 fj = fbuf[j];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const double dx = R.x[r] - xj, dy = R.y[r] - yj;
+        const double d2 = fma(dx, dx, dy * dy);
+        const double e = exp2_16<kMode>(d2, Kq0);
+        Tp[r] = fma(wj, e, Tp[r]);
+        if (kGrad) {
+          Vp[r] = fma(vj, e, Vp[r]);
+          Qp[r] = fma(wj, d2 * e, Qp[r]);  // z_j = w_j when q_j = 1
+        }
+      }
+    }
+  }
+  if (kTr && kVarying) {
+    // Density-scaled trigger, sparse: most pairs' spatial factor flushes to
+    // exactly 0.  Per 32-column chunk every lane first builds a bit mask of
+    // its live columns with an FP32 distance test against a conservatively
+    // rounded-up threshold (prep_kernel; a dead pair provably flushes), then
+    // pops its live columns lowest-first and evaluates only those in FP64.
+    // Each row still sums its columns in increasing j and only exact zeros
+    // are skipped, so the result is bitwise that of the dense loop.
+    for (int c = 0; c < kBJ; c += 32) {
+      unsigned mask[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) mask[r] = 0u;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) {
+        const float4 fj = fbuf[c + k];
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
           const float dxf = R.xf[r] - fj.x, dyf = R.yf[r] - fj.y;
-          go[r] = __any_sync(0xffffffffu, fmaf(dxf, dxf, dyf * dyf) <= fj.z);
+          if (fmaf(dxf, dxf, dyf * dyf) <= fj.z) mask[r] |= 1u << k;
         }
       }
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        if (kVarying && !go[r]) continue;
-        const double dx = R.x[r] - xj, dy = R.y[r] - yj;
-        const double d2 = fma(dx, dx, dy * dy);
-        const double e = exp2_16<kMode>(d2, Kj);
-        Tp[r] = fma(wj, e, Tp[r]);
-        if (kGrad) {
-          Vp[r] = fma(vj, e, Vp[r]);
-          Qp[r] = fma(zj, d2 * e, Qp[r]);
+        while (__any_sync(0xffffffffu, mask[r] != 0u)) {
+          if (mask[r]) {
+            const int j = c + __ffs(mask[r]) - 1;
+            mask[r] &= mask[r] - 1u;
+            const double dx = R.x[r] - sx[j], dy = R.y[r] - sy[j];
+            const double d2 = fma(dx, dx, dy * dy);
+            const double e = exp2_16<kMode>(d2, sk[j]);
+            Tp[r] = fma(sw[j], e, Tp[r]);
+            if (kGrad) {
+              Vp[r] = fma(sv[j], e, Vp[r]);
+              Qp[r] = fma(sz[j], d2 * e, Qp[r]);
+            }
+          }
         }
       }
     }
