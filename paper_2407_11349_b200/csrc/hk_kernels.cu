@@ -215,6 +215,24 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
     if (mask & (1u << s)) bulk_g2s(buf + s * kBJ, src[s] + j0, kBytes, bar);
 }
 
+// Squared FP32 distances of two rows (x0, y0), (x1, y1) to (xj, yj) with
+// packed f32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2).
+__device__ __forceinline__ float2 dist2_x2(float x0, float x1, float y0, float y1, float xj,
+                                           float yj) {
+  unsigned long long X, Y, XJ, YJ, dx, dy, d2;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(X) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(Y) : "f"(y0), "f"(y1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(XJ) : "f"(xj));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(YJ) : "f"(yj));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(X), "l"(XJ));
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(Y), "l"(YJ));
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(d2) : "l"(dy));
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d2) : "l"(dx), "l"(d2));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d2));
+  return r;
+}
+
 template <int R>
 struct RowState {
   double t[R], x[R], y[R];
@@ -281,13 +299,23 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
       unsigned mask[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) mask[r] = 0u;
-#pragma unroll 8
+#pragma unroll
       for (int k = 0; k < 32; ++k) {
         const float4 fj = fbuf[c + k];
+        if (NR % 2 == 0) {
+          // two rows per packed FP32x2 instruction (FADD2/FMUL2/FFMA2)
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const float dxf = R.xf[r] - fj.x, dyf = R.yf[r] - fj.y;
-          if (fmaf(dxf, dxf, dyf * dyf) <= fj.z) mask[r] |= 1u << k;
+          for (int r = 0; r < NR; r += 2) {
+            const float2 d2 = dist2_x2(R.xf[r], R.xf[r + 1], R.yf[r], R.yf[r + 1], fj.x, fj.y);
+            if (d2.x <= fj.z) mask[r] |= 1u << k;
+            if (d2.y <= fj.z) mask[r + 1] |= 1u << k;
+          }
+        } else {
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const float dxf = R.xf[r] - fj.x, dyf = R.yf[r] - fj.y;
+            if (fmaf(dxf, dxf, dyf * dyf) <= fj.z) mask[r] |= 1u << k;
+          }
         }
       }
 #pragma unroll
