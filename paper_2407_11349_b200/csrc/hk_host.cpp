@@ -141,7 +141,7 @@ std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g) 
   if (g == 0) throw std::invalid_argument("plan_shards: shard count must be positive");
   if (g > n) throw std::invalid_argument("plan_shards: more shards than rows");
   std::vector<double> cum(n + 1, 0.0);
-  const double row_bg = kCostAlpha * static_cast<double>(n - 1);
+  const double row_bg = background_cost(n) * static_cast<double>(n - 1);
   for (std::size_t i = 0; i < n; ++i) cum[i + 1] = cum[i] + row_bg + kCostBeta * lb[i];
   std::vector<std::size_t> b(g + 1, 0);
   b[g] = n;
@@ -183,9 +183,10 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
       double cost = 0.0;
       for (int J = tb; J < te; ++J) {
         const int j0 = J * kBJ, j1 = j0 + kBJ;
-        if (j1 <= lbmin) cost += kCostAlpha + kCostBeta;
-        else if (j0 >= ubmax && j1 <= n) cost += kCostAlpha;
-        else cost += kCostAlpha + kCostBeta + 8.0;
+        const double alpha = background_cost(static_cast<std::size_t>(n));
+        if (j1 <= lbmin) cost += alpha + kCostBeta;
+        else if (j0 >= ubmax && j1 <= n) cost += alpha;
+        else cost += kCostAlphaDirect + kCostBeta + 8.0;
       }
       cands.push_back({Item{r0, r1, tb, te, c, 0}, cost * (r1 - r0)});
     }

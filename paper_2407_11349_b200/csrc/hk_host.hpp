@@ -34,9 +34,18 @@ std::vector<std::size_t> partition_make(std::size_t n, std::size_t g);
 // count_before / upper_bound for every row of a sorted time array.
 void tie_bounds(const std::vector<double>& t, std::vector<int>& lb, std::vector<int>& ub);
 
-// Cost-balanced contiguous shards: row i costs kAlpha*(n-1) + kBeta*lb[i].
-constexpr double kCostAlpha = 13.0;  // FP64 instructions per background pair
-constexpr double kCostBeta = 17.0;   // FP64 instructions per trigger pair
+// Cost-balanced contiguous shards: row i costs alpha*(n-1) + kCostBeta*lb[i]
+// FP64 instructions (ncu-measured per-pair costs of the pair kernel).  The
+// background costs 13 per pair on the direct path but ~0.2 once the block
+// expansion qualifies, which it does for catalogs dense in time (large N);
+// alpha = background_cost(n) picks between the two.
+constexpr double kCostAlphaDirect = 13.0;    // FP64 per background pair, direct
+constexpr double kCostAlphaExpanded = 1.0;   // ... with the block expansion (rounded up)
+constexpr double kCostBeta = 16.0;           // FP64 per trigger pair
+constexpr std::size_t kExpansionRows = 32768;  // catalogs at least this large expand
+inline double background_cost(std::size_t n) {
+  return n >= kExpansionRows ? kCostAlphaExpanded : kCostAlphaDirect;
+}
 std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g);
 
 // Work items for rows [rb, re) of an n-event catalog: row blocks of

@@ -67,9 +67,16 @@ def test_plan_shards_balanced():
     for g in (1, 2, 4, 8):
         b = plan_shards(t, g)
         assert b[0] == 0 and b[-1] == len(t) and np.all(np.diff(b) > 0)
-        cost = 13.0 * (len(t) - 1) + 17.0 * lb
+        cost = 1.0 * (len(t) - 1) + 16.0 * lb  # N >= 32768: expanded background
         w = np.array([cost[b[i]:b[i + 1]].sum() for i in range(g)])
         assert w.max() / w.mean() < 1.001
+    # small catalogs (direct background) weigh the background at 13
+    ts = benchmark_catalog(5000, 3).t
+    lbs = np.searchsorted(ts, ts, side="left")
+    bs = plan_shards(ts, 4)
+    cs = 13.0 * (len(ts) - 1) + 16.0 * lbs
+    ws = np.array([cs[bs[i]:bs[i + 1]].sum() for i in range(4)])
+    assert ws.max() / ws.mean() < 1.01
     # the uniform partition is ~26% imbalanced at G=8
     u = np.linspace(0, len(t), 9).astype(int)
     wu = np.array([cost[u[i]:u[i + 1]].sum() for i in range(8)])
