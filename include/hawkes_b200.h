@@ -71,7 +71,10 @@ typedef struct hk_ctx hk_ctx;
  * uploads them to `n_gpus` devices (0..n_gpus-1; 0 means 1) and plans
  * cost-balanced row shards, one per device.  `density` is the per-event
  * population density (Event::density); the variant is chosen per
- * evaluation by hk_params.variant. */
+ * evaluation by hk_params.variant.  Non-finite locations are accepted (a
+ * coarse-only catalog, types.hpp:43-57 with coarse_only = true); evaluations
+ * then fail with HK_INVALID_ARGUMENT until hk_set_locations supplies finite
+ * ones (the cut posterior's X refresh). */
 int hk_create(const double* t, const double* lon, const double* lat, const double* density,
               size_t n, int n_gpus, hk_ctx** out);
 

@@ -103,6 +103,7 @@ struct hk_ctx {
   double d2_max = 0.0, q_max = 1.0;
   double cx = 0.0, cy = 0.0, half_extent = 0.0;
   bool unit_density = false;  // every density == 1: varying == constant exactly
+  bool locations_valid = true;  // false for a coarse-only catalog until set_locations
   std::vector<DeviceState> devs;
   bool profiling = false;
   int bg_expansion = 1;
@@ -150,6 +151,14 @@ struct hk_ctx {
   }
 
   void update_bbox() {
+    locations_valid = true;
+    for (int i = 0; i < n && locations_valid; ++i)
+      locations_valid = std::isfinite(x[i]) && std::isfinite(y[i]);
+    if (!locations_valid) {
+      d2_max = 0.0;
+      cx = cy = half_extent = 0.0;
+      return;
+    }
     double xmin = x[0], xmax = x[0], ymin = y[0], ymax = y[0];
     for (int i = 1; i < n; ++i) {
       xmin = std::min(xmin, x[i]);
@@ -230,6 +239,9 @@ struct hk_ctx {
 
   hk::EvalCoef coef(const hk_params* p, bool single = false) const {
     if (!p) throw std::invalid_argument("hk_eval: null params");
+    if (!locations_valid)
+      throw std::invalid_argument(
+          "hk_eval: event locations are not set (coarse-only catalog): call hk_set_locations first");
     hk::ParamsIn in{p->mu0, p->tau_t, p->xi0, p->sigma_x, p->sigma_t, p->area, p->variant};
     hk::validate_params(in);
     // With unit densities the varying kernel (q_j = D_j = 1) IS the constant
@@ -342,7 +354,10 @@ namespace {
 std::unique_ptr<hk_ctx> new_ctx(const double* t, const double* x, const double* y,
                                 const double* d, std::size_t n) {
   if (!t || !x || !y || !d) throw std::invalid_argument("hk_create: null array");
-  hk::validate_catalog(t, x, y, d, n);
+  // Non-finite locations are accepted (a coarse-only catalog, types.hpp:43,
+  // whose locations the cut posterior imputes); evaluation then requires
+  // hk_set_locations first.
+  hk::validate_catalog(t, x, y, d, n, /*coarse_only=*/true);
   auto ctx = std::make_unique<hk_ctx>();
   ctx->n = static_cast<int>(n);
   ctx->npad = static_cast<int>((n + hk::kBJ - 1) / hk::kBJ * hk::kBJ);

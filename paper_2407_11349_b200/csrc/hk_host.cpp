@@ -9,7 +9,7 @@
 namespace hk {
 
 void validate_catalog(const double* t, const double* x, const double* y, const double* d,
-                      std::size_t n) {
+                      std::size_t n, bool coarse_only) {
   if (n == 0) throw std::invalid_argument("Catalog: need at least one event");
   if (n >= (std::size_t{1} << 31) - 1024)
     throw std::invalid_argument("Catalog: more than 2^31 events is not supported");
@@ -19,7 +19,7 @@ void validate_catalog(const double* t, const double* x, const double* y, const d
     if (!(d[i] > 0.0))
       throw std::invalid_argument("Catalog: event " + std::to_string(i) +
                                   " has nonpositive density");
-    if (!std::isfinite(x[i]) || !std::isfinite(y[i]))
+    if (!coarse_only && (!std::isfinite(x[i]) || !std::isfinite(y[i])))
       throw std::invalid_argument("Catalog: event " + std::to_string(i) +
                                   " has non-finite location");
     if (i > 0 && t[i - 1] > t[i])

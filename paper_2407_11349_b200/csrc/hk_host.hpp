@@ -18,9 +18,10 @@ struct ParamsIn {
   int variant;
 };
 
-// Catalog invariants, types.hpp:43-57 (same checks, same messages).
+// Catalog invariants, types.hpp:43-57 (same checks, same messages);
+// coarse_only skips the location check (Catalog(events, coarse_only)).
 void validate_catalog(const double* t, const double* x, const double* y, const double* d,
-                      std::size_t n);
+                      std::size_t n, bool coarse_only = false);
 // HawkesParams::validate, types.hpp:92-103.
 void validate_params(const ParamsIn& p);
 

@@ -261,6 +261,59 @@ void sampler_unchanged() {
          same_chain && worst <= 1e-10, d);
 }
 
+void sampler_cut_unchanged() {
+  // the reference's cut-posterior sampler on a COARSE catalog (NaN locations,
+  // region ids only) with square county regions: resample_locations ->
+  // set_locations -> workspace evaluations, CPU workspace vs GPU workspace
+  RegionTable regions;
+  for (int gy = 0; gy < 4; ++gy)
+    for (int gx = 0; gx < 4; ++gx) {
+      const double x0 = -1.0 + 0.5 * gx, y0 = -1.0 + 0.5 * gy;
+      Region r;
+      r.id = "c" + std::to_string(4 * gy + gx);
+      r.polygons.push_back(PolygonShape{{{x0, y0}, {x0 + 0.5, y0}, {x0 + 0.5, y0 + 0.5}, {x0, y0 + 0.5}}, {}});
+      r.density = 1.0 + 50.0 * gx + 7.0 * gy;
+      r.representative_latitude = y0 + 0.25;
+      regions.add(std::move(r));
+    }
+  SimConfig sim;
+  sim.immigrant_rate = 3.0;
+  sim.horizon = 80.0;
+  sim.seed = 77;
+  sim.regions = &regions;
+  sim.variant = Variant::varying;
+  const Catalog fine = simulate_catalog(sim);
+  std::vector<Event> inside;
+  for (const Event& e : fine.events())
+    if (std::abs(e.lon) < 1.0 && std::abs(e.lat) < 1.0) inside.push_back(e);
+  const Catalog coarse = coarsen_catalog(Catalog(std::move(inside)), regions);
+  ChainConfig config;
+  config.iterations = 25;
+  config.burn_in = 5;
+  config.seed = 9;
+  config.initial.mu0 = 0.5;
+  config.initial.tau_t = 5.0;
+  config.initial.xi0 = 0.5;
+  config.initial.sigma_x = 0.1;
+  config.initial.sigma_t = 2.0;
+  config.initial.area = 4.0;
+  config.initial.variant = Variant::varying;
+  const ChainOutput cpu = run_cut_posterior(config, coarse, regions);
+  const ChainOutput gpu = dropin::cut_chain_b200(config, coarse, regions);
+  double draw_err = 0.0, ll_err = 0.0;
+  for (std::size_t i = 0; i < std::min(cpu.draws.size(), gpu.draws.size()); ++i) {
+    for (std::size_t k = 0; k < kParamCount; ++k)
+      draw_err = std::max(draw_err, std::abs(cpu.draws[i][k] - gpu.draws[i][k]) / std::abs(cpu.draws[i][k]));
+    ll_err = std::max(ll_err, std::abs(cpu.loglik_trace[i] - gpu.loglik_trace[i]) / std::abs(cpu.loglik_trace[i]));
+  }
+  const bool same = cpu.draws.size() == gpu.draws.size() && cpu.accepts == gpu.accepts &&
+                    draw_err <= 1e-12 && ll_err <= 1e-10;
+  char d[200];
+  std::snprintf(d, sizeof d, "coarse N=%zu, 16 counties, %zu draws, max draw rel diff %.3g, loglik %.3g",
+                coarse.size(), cpu.draws.size(), draw_err, ll_err);
+  report("mcmc.hpp cut-posterior sampler (coarse catalog) unchanged on the B200 workspace", same, d);
+}
+
 }  // namespace
 
 int main() {
@@ -270,6 +323,7 @@ int main() {
   criterion_2_single_finite();
   gradient_vs_fd();
   sampler_unchanged();
+  sampler_cut_unchanged();
   std::printf("%d failure(s)\n", failures);
   return failures;
 }

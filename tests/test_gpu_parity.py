@@ -416,3 +416,27 @@ def test_single_precision_adversarial_finite(eng):
             p = eng.HawkesParams(mu0=rng.uniform(0.1, 2), tau_t=rng.uniform(0.5, 20), xi0=rng.uniform(0.05, 0.9),
                                  sigma_x=rng.uniform(0.02, 0.5), sigma_t=rng.uniform(0.2, 10), area=1.0)
             assert np.isfinite(ev.eval_single(p))
+
+
+def test_coarse_catalog_needs_locations(eng):
+    """A coarse-only catalog (NaN locations, types.hpp:43) is accepted at
+    create; evaluation requires set_locations first (the cut posterior's X
+    refresh), after which it matches a fine catalog."""
+    import ctypes as C
+    from paper_2407_11349_b200._lib import lib, check
+    cat = eng.benchmark_catalog(2000, 4)
+    t, x, y, d = cat.arrays()
+    nan = np.full_like(x, np.nan)
+    h = C.c_void_p()
+    check(lib.hk_create(t, nan, nan, d, len(t), 1, C.byref(h)))
+    try:
+        p = eng.HawkesParams(**BENCH, variant=eng.Variant.varying).to_c()
+        ll = C.c_double()
+        assert lib.hk_eval(h, C.byref(p), C.byref(ll), None) == 1
+        assert b"locations are not set" in lib.hk_last_error()
+        check(lib.hk_set_locations(h, np.ascontiguousarray(x), np.ascontiguousarray(y)))
+        check(lib.hk_eval(h, C.byref(p), C.byref(ll), None))
+        want = eng.Evaluator(cat).eval(eng.HawkesParams(**BENCH, variant=eng.Variant.varying))
+        assert ll.value == want
+    finally:
+        lib.hk_destroy(h)
