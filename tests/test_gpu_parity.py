@@ -440,3 +440,22 @@ def test_coarse_catalog_needs_locations(eng):
         assert ll.value == want
     finally:
         lib.hk_destroy(h)
+
+
+def test_quadratic_scaling(eng):
+    """acceptance.cpp:115-124 (criterion 3) on the GPU: pair-kernel time grows
+    quadratically with N (log-log slope in [1.7, 2.3]) on the benchmark
+    catalog, LL + gradient, constant kernel."""
+    sizes = (100000, 200000, 400000)
+    times = []
+    p = eng.HawkesParams(**BENCH)
+    for n in sizes:
+        ev = eng.Evaluator(eng.benchmark_catalog(n, 42))
+        ev.eval(p, grad=True)
+        ev.set_profiling(True)
+        for _ in range(3):
+            ev.eval(p, grad=True)
+        ms, k, _ = ev.profile()
+        times.append(ms / k)
+    slope = np.polyfit(np.log(sizes), np.log(times), 1)[0]
+    assert 1.7 <= slope <= 2.3, (sizes, times, slope)
