@@ -59,7 +59,12 @@ __host__ __device__ constexpr int rows_per_item(bool varying) {
   return kThreads * rows_per_thread(varying);
 }
 // resident CTAs per SM the register budget is sized for (64K regs)
-__host__ __device__ constexpr int min_blocks(int rows) { return rows >= 4 ? 2 : (rows == 3 ? 2 : 4); }
+#ifndef HK_MIN_BLOCKS_CONST
+#define HK_MIN_BLOCKS_CONST 3
+#endif
+__host__ __device__ constexpr int min_blocks(int rows) {
+  return rows >= 4 ? HK_MIN_BLOCKS_CONST : (rows == 3 ? 2 : 4);
+}
 constexpr int kBJ = 256;                         // columns per shared-memory tile
 constexpr int kUnroll = HK_UNROLL;               // column-loop unroll of the fast tiles
 
