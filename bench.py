@@ -219,13 +219,13 @@ def run_ours(args):
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step():
+    def step(params=p):
         with torch.cuda.stream(stream):
             flush.zero_()
         if sh is not None:
-            sh.reduce(sh.partial_async(p, True))
+            sh.reduce(sh.partial_async(params, True))
         else:
-            ev.eval_async(p, True)
+            ev.eval_async(params, True)
 
     for _ in range(args.warmup):
         step()
@@ -278,6 +278,31 @@ def run_ours(args):
     if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     direct_ms_total, direct_pair_ms = float(t[0]), float(t[1])
+    # ---- the other kernel variant on the same catalog (config 4, the
+    # density-scaled lengthscale, when the headline is homogeneous)
+    other = "varying" if args.variant == "constant" else "constant"
+    p_other = HawkesParams(**BENCH_PARAMS, variant=Variant[other])
+    other_steps = 3
+    for _ in range(2):
+        step(p_other)
+    torch.cuda.synchronize()
+    ev.reset_profile()
+    ev.set_profiling(True)
+    o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        o0.record()
+    for _ in range(other_steps):
+        step(p_other)
+    with torch.cuda.stream(stream):
+        o1.record()
+    torch.cuda.synchronize()
+    opair_ms, opair_n, _ = ev.profile()
+    ev.set_profiling(False)
+    t = torch.tensor([o0.elapsed_time(o1), opair_ms / max(opair_n, 1)], dtype=torch.float64, device=dev)
+    if use_dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    other_ms_total, other_pair_ms = float(t[0]), float(t[1])
+
     # result of the last step, for the record
     if sh is not None:
         ll, g = sh.eval(p, grad=True)
@@ -371,6 +396,12 @@ def run_ours(args):
                 "roofline": {"bound": "fp64", "achieved": pairs_local * FP64_PER_PAIR * 2 / (direct_pair_ms * 1e-3) / 1e12,
                              "peak": fp64_peak, "unit": "TFLOP/s",
                              "frac": pairs_local * FP64_PER_PAIR * 2 / (direct_pair_ms * 1e-3) / 1e12 / fp64_peak}},
+            ("density_scaled" if other == "varying" else "homogeneous"): {
+                "note": f"the same LL+grad step with the {other} kernel on the same catalog "
+                        f"(BASELINE config {4 if other == 'varying' else 3}), device-timed like `value`",
+                "variant": other, "value": other_steps / (other_ms_total * 1e-3), "unit": "evals/s",
+                "ms_per_step": other_ms_total / other_steps, "pair_kernel_ms": other_pair_ms,
+                "pairs_per_sec": other_steps / (other_ms_total * 1e-3) * pairs},
             "cpu_baseline": cpu,
             "clocks": clk,
             "result": {"loglik": ll, "grad": [float(x) for x in g]},

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -60,6 +61,14 @@ int guarded(Fn&& fn) {
   }
 }
 
+// Row blocks per clustering window of the varying plan (HK_ROW_WINDOW
+// overrides; 1 disables the clustering).
+int row_window() {
+  const char* e = std::getenv("HK_ROW_WINDOW");
+  const int w = e ? std::atoi(e) : 8;
+  return (w == 1 || w == 2 || w == 4 || w == 8) ? w : 8;
+}
+
 template <typename T>
 T* dmalloc(std::size_t count) {
   void* p = nullptr;
@@ -76,6 +85,11 @@ struct DeviceState {
   float4* fxy = nullptr;
   float2* fkw = nullptr;
   int *lb = nullptr, *ub = nullptr;
+  // clustered row order of the varying plan (hk::launch_cluster), valid for
+  // location version rperm_loc
+  int* rperm = nullptr;
+  int window = 1;
+  long rperm_loc = -1;
   // work plans per variant (rows per item differ, hk_device.cuh)
   hk::Item* items[2] = {nullptr, nullptr};
   int n_items[2] = {0, 0}, slots[2] = {0, 0};
@@ -90,7 +104,7 @@ struct DeviceState {
   std::size_t prof_used = 0;
 
   hk::DeviceCatalog catalog(int n, int npad) const {
-    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z, fxy, fkw};
+    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z, fxy, fkw, rperm};
   }
 };
 
@@ -139,6 +153,7 @@ struct hk_ctx {
       if (s.fkw) cudaFree(s.fkw);
       if (s.lb) cudaFree(s.lb);
       if (s.ub) cudaFree(s.ub);
+      if (s.rperm) cudaFree(s.rperm);
       for (hk::Item* it : s.items)
         if (it) cudaFree(it);
       if (s.h_out6) cudaFreeHost(s.h_out6);
@@ -206,9 +221,17 @@ struct hk_ctx {
     upload_padded(s, s.q, d, 1.0);
     ck(cudaMemcpy(s.lb, lb.data(), n * sizeof(int), cudaMemcpyHostToDevice), "upload lb");
     ck(cudaMemcpy(s.ub, ub.data(), n * sizeof(int), cudaMemcpyHostToDevice), "upload ub");
+    // The varying kernel reads its rows in spatially clustered windows of
+    // kRowWindow row blocks so that warps can skip columns (launch_cluster).
+    s.window = row_window();
+    if (s.window > 1) {
+      const int wr = s.window * hk::rows_per_item(true);
+      s.rperm = dmalloc<int>(static_cast<std::size_t>((re - rb + wr - 1) / wr) * wr);
+    }
     for (int v = 0; v < 2; ++v) {
       std::vector<hk::Item> items;
-      s.slots[v] = hk::plan_items(lb, ub, n, rb, re, hk::rows_per_item(v != 0), items);
+      s.slots[v] = hk::plan_items(lb, ub, n, rb, re, hk::rows_per_item(v != 0), items,
+                                  v != 0 ? s.window : 1);
       s.n_items[v] = static_cast<int>(items.size());
       s.items[v] = dmalloc<hk::Item>(items.size());
       ck(cudaMemcpy(s.items[v], items.data(), items.size() * sizeof(hk::Item),
@@ -303,6 +326,12 @@ struct hk_ctx {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const hk::DeviceCatalog dc = s.catalog(n, npad);
     const int rows = s.re - s.rb;
+    if (c.varying && s.window > 1 && s.rperm_loc != loc_version) {
+      hk::launch_cluster(s.x, s.y, s.rperm, s.rb, rows, s.window * hk::rows_per_item(true),
+                         32 * hk::rows_per_thread(true), c.cx, c.cy, s.stream);
+      s.rperm_loc = loc_version;
+      prof_total += 1;
+    }
     if (halves) {
       hk::launch_prep(dc, c, s.stream);
       std::pair<cudaEvent_t, cudaEvent_t> ev{};

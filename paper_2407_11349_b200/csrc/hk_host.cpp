@@ -156,11 +156,12 @@ std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g) 
 }
 
 int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
-               int kBI, std::vector<Item>& items) {
+               int kBI, std::vector<Item>& items, int window) {
   items.clear();
   const int npad = (n + kBJ - 1) / kBJ * kBJ;
   const int ntiles = npad / kBJ;
   const int nblocks = (re - rb + kBI - 1) / kBI;
+  const int G = std::max(1, window);
   // Enough items to keep every SM busy for many waves (148 SMs x 4 CTAs x
   // 16) and none larger than ~2^25 pair terms, capped at one tile each.
   const double pairs_per_block = static_cast<double>(std::min(kBI, re - rb)) * n;
@@ -176,8 +177,13 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
   std::vector<Cand> cands;
   cands.reserve(static_cast<std::size_t>(nblocks) * slots);
   for (int b = 0; b < nblocks; ++b) {
+    // the block's own rows [r0, r1) and the rows [w0, w1) it is classified
+    // against (its window)
     const int r0 = rb + b * kBI, r1 = std::min(re, r0 + kBI);
-    const int lbmin = lb[r0], ubmax = ub[r1 - 1];
+    const int w0 = G > 1 ? rb + (b / G) * G * kBI : r0;
+    const int w1 = G > 1 ? std::min(re, w0 + G * kBI) : r1;
+    const int pos = G > 1 ? r0 - rb : -1;
+    const int lbmin = lb[w0], ubmax = ub[w1 - 1];
     for (int c = 0; c < slots; ++c) {
       const int tb = c * per, te = std::min(ntiles, (c + 1) * per);
       double cost = 0.0;
@@ -188,7 +194,7 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
         else if (j0 >= ubmax && j1 <= n) cost += alpha;
         else cost += kCostAlphaDirect + kCostBeta + 8.0;
       }
-      cands.push_back({Item{r0, r1, tb, te, c, 0}, cost * (r1 - r0)});
+      cands.push_back({Item{w0, w1, tb, te, c, pos}, cost * (r1 - r0)});
     }
   }
   std::stable_sort(cands.begin(), cands.end(),

@@ -51,9 +51,12 @@ std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g);
 
 // Work items for rows [rb, re) of an n-event catalog: row blocks of
 // rows_per_item rows times column chunks of whole tiles; heaviest first.  Returns the
-// number of chunk slots per row.
+// number of chunk slots per row.  window > 1: the rows are taken in windows
+// of window * rows_per_item rows, classified against the whole window and
+// read through the clustered order rperm[(window start - rb) + ...]
+// (Item::pos; launch_cluster with the same window).
 int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
-               int rows_per_item, std::vector<Item>& items);
+               int rows_per_item, std::vector<Item>& items, int window = 1);
 
 // Per-evaluation coefficients (types.hpp:105-109, model.hpp:328-336) and
 // the host-side argument bound that selects the checked exp.

@@ -237,9 +237,25 @@ template <int R>
 struct RowState {
   double t[R], x[R], y[R];
   float xf[R], yf[R];  // FP32 coordinates in the skip-test frame (varying)
+  float bx0, bx1, by0, by1;  // FP32 bounding box of the warp's rows (warp-uniform)
   int lb[R], ub[R];
   double B[R], B2[R], T[R], Td[R], Tq[R];
 };
+
+// Columns c .. c+31 that may have a live pair with some row of this warp
+// (warp-uniform bit mask; lane k tests column c + k).  The squared FP32
+// distance from a column to the warp's bounding box is computed with the
+// same roundings as the per-pair test (dist2_x2) and FP32 subtraction,
+// squaring and fma are monotone, so it never exceeds any row's pair
+// distance: a column outside the mask fails the pair test for every row.
+template <int NR>
+__device__ __forceinline__ unsigned warp_candidates(const RowState<NR>& R,
+                                                    const float4* __restrict__ fbuf, int c) {
+  const float4 f = fbuf[c + (threadIdx.x & 31)];
+  const float ex = fmaxf(fmaxf(R.bx0 - f.x, f.x - R.bx1), 0.f);
+  const float ey = fmaxf(fmaxf(R.by0 - f.y, f.y - R.by1), 0.f);
+  return __ballot_sync(0xffffffffu, fmaf(ex, ex, ey * ey) <= f.z);
+}
 
 // BT / B / T tiles: no per-pair guards.
 template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr>
@@ -296,11 +312,14 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
     // Each row still sums its columns in increasing j and only exact zeros
     // are skipped, so the result is bitwise that of the dense loop.
     for (int c = 0; c < kBJ; c += 32) {
+      unsigned cand = warp_candidates(R, fbuf, c);
+      if (cand == 0u) continue;
       unsigned mask[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) mask[r] = 0u;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) {
+      while (cand) {  // warp-uniform
+        const int k = __ffs(cand) - 1;
+        cand &= cand - 1u;
         const float4 fj = fbuf[c + k];
         if (NR % 2 == 0) {
           // two rows per packed FP32x2 instruction (FADD2/FMUL2/FFMA2)
@@ -369,16 +388,35 @@ __device__ __forceinline__ void tile_trig_f32(RowState<NR>& R, const double* __r
   float Tp[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) Tp[r] = 0.f;
-#pragma unroll 4
-  for (int j = 0; j < kBJ; ++j) {
-    const float4 fj = fbuf[j];
-    const float2 kw = kwbuf[j];
+  if (kVarying) {
+    // only the warp's candidate columns (warp_candidates); the others add
+    // exact zeros to every row
+    for (int c = 0; c < kBJ; c += 32) {
+      unsigned cand = warp_candidates(R, fbuf, c);
+      while (cand) {
+        const int j = c + __ffs(cand) - 1;
+        cand &= cand - 1u;
+        const float4 fj = fbuf[j];
+        const float2 kw = kwbuf[j];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const float dx = R.xf[r] - fj.x, dy = R.yf[r] - fj.y;
-      const float d2 = fmaf(dx, dx, dy * dy);
-      if (kVarying && !__any_sync(0xffffffffu, d2 <= fj.z)) continue;
-      Tp[r] = fmaf(kw.y, ex2_approx(d2 * kw.x), Tp[r]);
+        for (int r = 0; r < NR; ++r) {
+          const float dx = R.xf[r] - fj.x, dy = R.yf[r] - fj.y;
+          const float d2 = fmaf(dx, dx, dy * dy);
+          if (!__any_sync(0xffffffffu, d2 <= fj.z)) continue;
+          Tp[r] = fmaf(kw.y, ex2_approx(d2 * kw.x), Tp[r]);
+        }
+      }
+    }
+  } else {
+#pragma unroll 4
+    for (int j = 0; j < kBJ; ++j) {
+      const float4 fj = fbuf[j];
+      const float2 kw = kwbuf[j];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const float dx = R.xf[r] - fj.x, dy = R.yf[r] - fj.y;
+        Tp[r] = fmaf(kw.y, ex2_approx(fmaf(dx, dx, dy * dy) * kw.x), Tp[r]);
+      }
     }
   }
   const double t_ref = st[kBJ - 1];
@@ -538,11 +576,23 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
 
   RowState<NR> R;
   bool valid[NR];
+  // Varying: row r of a thread is position warp * 32 NR + r * 32 + lane,
+  // so each warp holds 32 NR consecutive positions (one cluster when the
+  // item's rows are permuted).  Constant: rows rb + tid + r * kThreads.
+  const int pos0 = kVarying ? (tid >> 5) * (32 * NR) + (tid & 31) : tid;
+  constexpr int kPosStride = kVarying ? 32 : kThreads;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    int row = it.rb + tid + r * kThreads;
-    valid[r] = row < it.re;
-    row = valid[r] ? row : it.re - 1;
+    int row;
+    if (kVarying && it.pos >= 0) {
+      row = P.d.rperm[it.pos + pos0 + r * kPosStride];
+      valid[r] = row >= 0;
+      row = valid[r] ? row : it.rb;
+    } else {
+      row = it.rb + pos0 + r * kPosStride;
+      valid[r] = row < it.re;
+      row = valid[r] ? row : it.re - 1;
+    }
     R.t[r] = P.d.t[row];
     R.x[r] = P.d.x[row];
     R.y[r] = P.d.y[row];
@@ -551,6 +601,27 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     R.lb[r] = P.d.lb[row];
     R.ub[r] = P.d.ub[row];
     R.B[r] = R.B2[r] = R.T[r] = R.Td[r] = R.Tq[r] = 0.0;
+  }
+  if (kVarying) {
+    float x0 = R.xf[0], x1 = R.xf[0], y0 = R.yf[0], y1 = R.yf[0];
+#pragma unroll
+    for (int r = 1; r < NR; ++r) {
+      x0 = fminf(x0, R.xf[r]);
+      x1 = fmaxf(x1, R.xf[r]);
+      y0 = fminf(y0, R.yf[r]);
+      y1 = fmaxf(y1, R.yf[r]);
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+      x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+      y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, off));
+      y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+    }
+    R.bx0 = x0;
+    R.bx1 = x1;
+    R.by0 = y0;
+    R.by1 = y1;
   }
   __syncthreads();
 
@@ -625,7 +696,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     if (!valid[r]) continue;
-    const size_t i = static_cast<size_t>(it.rb + tid + r * kThreads - P.rows_base);
+    const int row = (kVarying && it.pos >= 0) ? P.d.rperm[it.pos + pos0 + r * kPosStride]
+                                              : it.rb + pos0 + r * kPosStride;
+    const size_t i = static_cast<size_t>(row - P.rows_base);
     out[0 * plane + i] = R.B[r];
     out[1 * plane + i] = R.B2[r];
     out[2 * plane + i] = R.T[r];
@@ -668,6 +741,58 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
     d.v[j] = 0.0;
     d.z[j] = 0.0;
   }
+}
+
+// ---------------------------------------------------------------------------
+// row clustering (varying kernel): one CTA per row window
+
+constexpr int kClusterThreads = 1024;
+constexpr int kMaxWindow = 2048;
+
+// k-d median splits by sorting: the window is sorted by x, each half by y,
+// each quarter by x, ... down to `leaf` rows (one warp's rows).  Every
+// segment ends ascending, so the padding entries (keys +inf, row -1) end up
+// at the window's tail at every level.
+__global__ void __launch_bounds__(kClusterThreads)
+    cluster_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm,
+                   int rows_base, int rows, int window, int leaf, double cx, double cy) {
+  __shared__ float kx[kMaxWindow], ky[kMaxWindow];
+  __shared__ int kv[kMaxWindow];
+  const int w0 = blockIdx.x * window;
+  for (int i = threadIdx.x; i < window; i += kClusterThreads) {
+    const int li = w0 + i;
+    const bool ok = li < rows;
+    kx[i] = ok ? __double2float_rn(x[rows_base + li] - cx) : __int_as_float(0x7f800000);
+    ky[i] = ok ? __double2float_rn(y[rows_base + li] - cy) : __int_as_float(0x7f800000);
+    kv[i] = ok ? rows_base + li : -1;
+  }
+  __syncthreads();
+  int level = 0;
+  for (int S = window; S > leaf; S >>= 1, ++level) {
+    const float* key = (level & 1) ? ky : kx;
+    for (int k = 2; k <= S; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < window; i += kClusterThreads) {
+          const int l = i ^ j;
+          if (l > i) {
+            const bool up = k == S || (i & k) == 0;
+            if ((key[i] > key[l]) == up) {
+              const float ax = kx[i], ay = ky[i];
+              const int av = kv[i];
+              kx[i] = kx[l];
+              ky[i] = ky[l];
+              kv[i] = kv[l];
+              kx[l] = ax;
+              ky[l] = ay;
+              kv[l] = av;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  for (int i = threadIdx.x; i < window; i += kClusterThreads) rperm[w0 + i] = kv[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -809,6 +934,14 @@ void launch_pair_t(const PairParams& P, int n_items, cudaStream_t s) {
 void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
   const int threads = 256;
   prep_kernel<<<(d.npad + threads - 1) / threads, threads, 0, s>>>(d, c);
+}
+
+void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
+                    int window, int leaf, double cx, double cy, cudaStream_t s) {
+  if (rows <= 0 || window > kMaxWindow || window < leaf) return;
+  const int windows = (rows + window - 1) / window;
+  cluster_kernel<<<windows, kClusterThreads, 0, s>>>(x, y, rperm, rows_base, rows, window, leaf, cx,
+                                                     cy);
 }
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,

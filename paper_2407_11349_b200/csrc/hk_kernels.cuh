@@ -8,10 +8,14 @@
 
 namespace hk {
 
-// One work item = one CTA: rows [rb, re) (<= kBI rows) against column tiles
-// [tb, te); its five per-row partial sums land in partial slot `slot`.
+// One work item = one CTA: up to kBI rows against column tiles [tb, te);
+// its five per-row partial sums land in partial slot `slot`.  [rb, re) is
+// the row block the column tiles are classified against.  pos < 0: the rows
+// are rb, rb+1, ... (< re).  pos >= 0: the rows are rperm[pos .. pos+kBI)
+// (-1 = none), a spatially clustered order of a row window (cluster_kernel)
+// in which each warp's 32*NR consecutive positions form one cluster.
 struct Item {
-  int rb, re, tb, te, slot, pad;
+  int rb, re, tb, te, slot, pos;
 };
 
 // Per-evaluation coefficients, all derived on the host in double exactly
@@ -52,12 +56,20 @@ struct DeviceCatalog {
   double* z;         // prep: q_j w_j                                 [npad]
   float4* fxy;       // prep: {x_j - cx, y_j - cy, thrf_j, 0} in FP32     [npad]
   float2* fkw;       // prep: {K_j log2(e)/(ln2-units), w_j} in FP32 (single precision) [npad]
+  const int* rperm;  // clustered row order per row window (Item::pos), or null
 };
 
 // Row-sum halves: the background [B, B2] and the trigger [T, Td, Tq].
 constexpr int kHalfBg = 1, kHalfTr = 2;
 
 void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
+// Spatially clusters the rows [rows_base, rows_base + rows) window by window
+// (window rows each, k-d median splits down to `leaf` rows) into rperm;
+// positions past the last row hold -1.  Any order gives bitwise the same
+// per-row sums: the clustering only lets the density-scaled trigger skip
+// columns per warp.
+void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
+                    int window, int leaf, double cx, double cy, cudaStream_t s);
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
                  double* partial, int rows_base, int rows_total, bool with_grad, int halves,
                  cudaStream_t s);
