@@ -248,13 +248,23 @@ struct RowState {
 // same roundings as the per-pair test (dist2_x2) and FP32 subtraction,
 // squaring and fma are monotone, so it never exceeds any row's pair
 // distance: a column outside the mask fails the pair test for every row.
+// With `wide`, also the candidates whose threshold disc covers the warp's
+// whole box (squared distance to the farthest corner within the threshold):
+// those are live for (nearly) every row and are evaluated densely.
 template <int NR>
 __device__ __forceinline__ unsigned warp_candidates(const RowState<NR>& R,
-                                                    const float4* __restrict__ fbuf, int c) {
+                                                    const float4* __restrict__ fbuf, int c,
+                                                    unsigned* wide = nullptr) {
   const float4 f = fbuf[c + (threadIdx.x & 31)];
   const float ex = fmaxf(fmaxf(R.bx0 - f.x, f.x - R.bx1), 0.f);
   const float ey = fmaxf(fmaxf(R.by0 - f.y, f.y - R.by1), 0.f);
-  return __ballot_sync(0xffffffffu, fmaf(ex, ex, ey * ey) <= f.z);
+  const bool near = fmaf(ex, ex, ey * ey) <= f.z;
+  if (wide) {
+    const float fx = fmaxf(f.x - R.bx0, R.bx1 - f.x);
+    const float fy = fmaxf(f.y - R.by0, R.by1 - f.y);
+    *wide = __ballot_sync(0xffffffffu, near && fmaf(fx, fx, fy * fy) <= f.z);
+  }
+  return __ballot_sync(0xffffffffu, near);
 }
 
 // BT / B / T tiles: no per-pair guards.
@@ -305,14 +315,36 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
   }
   if (kTr && kVarying) {
     // Density-scaled trigger, sparse: most pairs' spatial factor flushes to
-    // exactly 0.  Per 32-column chunk every lane first builds a bit mask of
-    // its live columns with an FP32 distance test against a conservatively
-    // rounded-up threshold (prep_kernel; a dead pair provably flushes), then
-    // pops its live columns lowest-first and evaluates only those in FP64.
-    // Each row still sums its columns in increasing j and only exact zeros
-    // are skipped, so the result is bitwise that of the dense loop.
+    // exactly 0.  Per 32-column chunk the warp first classifies the columns
+    // against its rows' bounding box (warp_candidates): columns out of reach
+    // are dropped, columns whose reach covers the whole box ("wide") are
+    // evaluated densely for every row.  For the remaining candidates every
+    // lane builds a bit mask of its live columns with an FP32 distance test
+    // against a conservatively rounded-up threshold (prep_kernel; a dead
+    // pair provably flushes), then pops its live columns lowest-first and
+    // evaluates only those in FP64.  Only exact zeros are skipped; each row
+    // sums its wide columns, then its popped columns, in increasing j.
     for (int c = 0; c < kBJ; c += 32) {
-      unsigned cand = warp_candidates(R, fbuf, c);
+      unsigned wide;
+      unsigned cand = warp_candidates(R, fbuf, c, &wide);
+      if (cand == 0u) continue;
+      cand &= ~wide;
+      while (wide) {  // warp-uniform, dense
+        const int j = c + __ffs(wide) - 1;
+        wide &= wide - 1u;
+        const double xj = sx[j], yj = sy[j], kj = sk[j], wj = sw[j];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const double dx = R.x[r] - xj, dy = R.y[r] - yj;
+          const double d2 = fma(dx, dx, dy * dy);
+          const double e = exp2_16<kMode>(d2, kj);
+          Tp[r] = fma(wj, e, Tp[r]);
+          if (kGrad) {
+            Vp[r] = fma(sv[j], e, Vp[r]);
+            Qp[r] = fma(sz[j], d2 * e, Qp[r]);
+          }
+        }
+      }
       if (cand == 0u) continue;
       unsigned mask[NR];
 #pragma unroll
