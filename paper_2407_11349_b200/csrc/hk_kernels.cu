@@ -215,24 +215,6 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
     if (mask & (1u << s)) bulk_g2s(buf + s * kBJ, src[s] + j0, kBytes, bar);
 }
 
-// Squared FP32 distances of two rows (x0, y0), (x1, y1) to (xj, yj) with
-// packed f32x2 arithmetic (sm_100: FADD2 / FMUL2 / FFMA2).
-__device__ __forceinline__ float2 dist2_x2(float x0, float x1, float y0, float y1, float xj,
-                                           float yj) {
-  unsigned long long X, Y, XJ, YJ, dx, dy, d2;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(X) : "f"(x0), "f"(x1));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(Y) : "f"(y0), "f"(y1));
-  asm("mov.b64 %0, {%1, %1};" : "=l"(XJ) : "f"(xj));
-  asm("mov.b64 %0, {%1, %1};" : "=l"(YJ) : "f"(yj));
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dx) : "l"(X), "l"(XJ));
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dy) : "l"(Y), "l"(YJ));
-  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(d2) : "l"(dy));
-  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d2) : "l"(dx), "l"(d2));
-  float2 r;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d2));
-  return r;
-}
-
 template <int R>
 struct RowState {
   double t[R], x[R], y[R];
@@ -243,28 +225,20 @@ struct RowState {
 };
 
 // Columns c .. c+31 that may have a live pair with some row of this warp
-// (warp-uniform bit mask; lane k tests column c + k).  The squared FP32
-// distance from a column to the warp's bounding box is computed with the
-// same roundings as the per-pair test (dist2_x2) and FP32 subtraction,
-// squaring and fma are monotone, so it never exceeds any row's pair
-// distance: a column outside the mask fails the pair test for every row.
-// With `wide`, also the candidates whose threshold disc covers the warp's
-// whole box (squared distance to the farthest corner within the threshold):
-// those are live for (nearly) every row and are evaluated densely.
+// (warp-uniform bit mask; lane k tests column c + k).  prep_kernel rounds
+// each column's threshold up so that an FP32 pair distance
+// fmaf(dx, dx, dy*dy), dx = xf_i - xf_j, above it implies an exact
+// distance beyond the flush threshold.  The box distance below uses the same
+// FP32 operations on the box edges; they are monotone, so it never exceeds
+// any row's FP32 pair distance: a column outside the mask flushes to exactly
+// 0 for every row of the warp.
 template <int NR>
 __device__ __forceinline__ unsigned warp_candidates(const RowState<NR>& R,
-                                                    const float4* __restrict__ fbuf, int c,
-                                                    unsigned* wide = nullptr) {
+                                                    const float4* __restrict__ fbuf, int c) {
   const float4 f = fbuf[c + (threadIdx.x & 31)];
   const float ex = fmaxf(fmaxf(R.bx0 - f.x, f.x - R.bx1), 0.f);
   const float ey = fmaxf(fmaxf(R.by0 - f.y, f.y - R.by1), 0.f);
-  const bool near = fmaf(ex, ex, ey * ey) <= f.z;
-  if (wide) {
-    const float fx = fmaxf(f.x - R.bx0, R.bx1 - f.x);
-    const float fy = fmaxf(f.y - R.by0, R.by1 - f.y);
-    *wide = __ballot_sync(0xffffffffu, near && fmaf(fx, fx, fy * fy) <= f.z);
-  }
-  return __ballot_sync(0xffffffffu, near);
+  return __ballot_sync(0xffffffffu, fmaf(ex, ex, ey * ey) <= f.z);
 }
 
 // BT / B / T tiles: no per-pair guards.
@@ -314,25 +288,21 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
     }
   }
   if (kTr && kVarying) {
-    // Density-scaled trigger, sparse: most pairs' spatial factor flushes to
-    // exactly 0.  Per 32-column chunk the warp first classifies the columns
-    // against its rows' bounding box (warp_candidates): columns out of reach
-    // are dropped, columns whose reach covers the whole box ("wide") are
-    // evaluated densely for every row.  For the remaining candidates every
-    // lane builds a bit mask of its live columns with an FP32 distance test
-    // against a conservatively rounded-up threshold (prep_kernel; a dead
-    // pair provably flushes), then pops its live columns lowest-first and
-    // evaluates only those in FP64.  Only exact zeros are skipped; each row
-    // sums its wide columns, then its popped columns, in increasing j.
+    // Density-scaled trigger: most pairs' spatial factor flushes to exactly
+    // 0.  Per 32-column chunk the warp keeps only the columns that can reach
+    // its rows' bounding box (warp_candidates, a conservative FP32 test
+    // against a rounded-up threshold: a dropped column provably flushes for
+    // every row of the warp) and evaluates those densely.  The rows arrive
+    // spatially clustered (cluster_kernel), so the boxes are small.  Only
+    // exact zeros are skipped and each row still sums in increasing j: the
+    // result is bitwise that of the dense loop.
     for (int c = 0; c < kBJ; c += 32) {
-      unsigned wide;
-      unsigned cand = warp_candidates(R, fbuf, c, &wide);
-      if (cand == 0u) continue;
-      cand &= ~wide;
-      while (wide) {  // warp-uniform, dense
-        const int j = c + __ffs(wide) - 1;
-        wide &= wide - 1u;
+      unsigned cand = warp_candidates(R, fbuf, c);
+      while (cand) {  // warp-uniform
+        const int j = c + __ffs(cand) - 1;
+        cand &= cand - 1u;
         const double xj = sx[j], yj = sy[j], kj = sk[j], wj = sw[j];
+        const double vj = kGrad ? sv[j] : 0.0, zj = kGrad ? sz[j] : 0.0;
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
           const double dx = R.x[r] - xj, dy = R.y[r] - yj;
@@ -340,49 +310,8 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
           const double e = exp2_16<kMode>(d2, kj);
           Tp[r] = fma(wj, e, Tp[r]);
           if (kGrad) {
-            Vp[r] = fma(sv[j], e, Vp[r]);
-            Qp[r] = fma(sz[j], d2 * e, Qp[r]);
-          }
-        }
-      }
-      if (cand == 0u) continue;
-      unsigned mask[NR];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) mask[r] = 0u;
-      while (cand) {  // warp-uniform
-        const int k = __ffs(cand) - 1;
-        cand &= cand - 1u;
-        const float4 fj = fbuf[c + k];
-        if (NR % 2 == 0) {
-          // two rows per packed FP32x2 instruction (FADD2/FMUL2/FFMA2)
-#pragma unroll
-          for (int r = 0; r < NR; r += 2) {
-            const float2 d2 = dist2_x2(R.xf[r], R.xf[r + 1], R.yf[r], R.yf[r + 1], fj.x, fj.y);
-            if (d2.x <= fj.z) mask[r] |= 1u << k;
-            if (d2.y <= fj.z) mask[r + 1] |= 1u << k;
-          }
-        } else {
-#pragma unroll
-          for (int r = 0; r < NR; ++r) {
-            const float dxf = R.xf[r] - fj.x, dyf = R.yf[r] - fj.y;
-            if (fmaf(dxf, dxf, dyf * dyf) <= fj.z) mask[r] |= 1u << k;
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        while (__any_sync(0xffffffffu, mask[r] != 0u)) {
-          if (mask[r]) {
-            const int j = c + __ffs(mask[r]) - 1;
-            mask[r] &= mask[r] - 1u;
-            const double dx = R.x[r] - sx[j], dy = R.y[r] - sy[j];
-            const double d2 = fma(dx, dx, dy * dy);
-            const double e = exp2_16<kMode>(d2, sk[j]);
-            Tp[r] = fma(sw[j], e, Tp[r]);
-            if (kGrad) {
-              Vp[r] = fma(sv[j], e, Vp[r]);
-              Qp[r] = fma(sz[j], d2 * e, Qp[r]);
-            }
+            Vp[r] = fma(vj, e, Vp[r]);
+            Qp[r] = fma(zj, d2 * e, Qp[r]);
           }
         }
       }
@@ -779,7 +708,7 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
 // row clustering (varying kernel): one CTA per row window
 
 constexpr int kClusterThreads = 1024;
-constexpr int kMaxWindow = 2048;
+constexpr int kMaxWindow = 4096;
 
 // k-d median splits by sorting: the window is sorted by x, each half by y,
 // each quarter by x, ... down to `leaf` rows (one warp's rows).  Every
