@@ -167,6 +167,7 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
   const double pairs_per_block = static_cast<double>(std::min(kBI, re - rb)) * n;
   int slots = static_cast<int>(std::ceil(pairs_per_block / double(1 << 25)));
   slots = std::max(slots, (148 * 4 * 16 + nblocks - 1) / nblocks);
+  slots = std::max(slots, (ntiles + kMaxItemTiles - 1) / kMaxItemTiles);
   slots = std::max(1, std::min(slots, ntiles));
   const int per = (ntiles + slots - 1) / slots;
   slots = (ntiles + per - 1) / per;

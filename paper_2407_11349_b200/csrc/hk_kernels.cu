@@ -142,10 +142,9 @@ __device__ __forceinline__ int tile_type_all(int J, const BlockInfo& bi, const P
 // background-only launch turns BT/BTx into B/Bx and skips T tiles; a
 // trigger-only launch turns BT/BTx into T and skips B/Bx tiles.  M tiles
 // compute both halves (one per row block; the unused half is discarded).
-__device__ __forceinline__ int tile_type(int J, const BlockInfo& bi, const PairParams& P) {
-  const int t = tile_type_all(J, bi, P);
-  if (P.halves == (kHalfBg | kHalfTr) || t == kTileM || t == kSkip) return t;
-  if (P.halves == kHalfBg) {
+__device__ __forceinline__ int restrict_type(int t, int halves) {
+  if (halves == (kHalfBg | kHalfTr) || t == kTileM || t == kSkip) return t;
+  if (halves == kHalfBg) {
     if (t == kTileBT) return kTileB;
     if (t == kTileBTx) return kTileBx;
     return t == kTileT ? kSkip : t;
@@ -400,10 +399,8 @@ __device__ __forceinline__ void bg_expansion(RowState<NR>& R, const double* __re
   const double cJ = 0.5 * (st[0] + st[ncols - 1]);
   const double D = s * (cI - cJ);
   const double eps = 0.5 * s * s * (bi.t_last - bi.t_first) * (st[ncols - 1] - st[0]);
-  int P = 2;  // smallest number of terms with eps^(P+1)/(P+1)! <= 2^-64 (uniform)
-  for (double rem = eps * eps * eps / 6.0; P < kXP && rem > 5.421010862427522e-20; ++P)
-    rem *= eps / (P + 2);
-  const int nm = P + (kGrad ? 3 : 1);
+  (void)eps;  // <= kEpsMax by expansion_ok: kXP terms leave a remainder < 4e-21
+  constexpr int nm = kXP + (kGrad ? 3 : 1);
   double m[kNM];
 #pragma unroll
   for (int n = 0; n < kNM; ++n) m[n] = 0.0;
@@ -442,23 +439,14 @@ __device__ __forceinline__ void bg_expansion(RowState<NR>& R, const double* __re
     const double alpha = s * (R.t[r] - cI);
     const double gamma = D + alpha;
     const double x = 2.0 * alpha;
-    double S0 = m[kXP], S1 = m[kXP + 1], S2 = m[kXP + 2];
+    double S0 = m[kXP], S1 = kGrad ? m[kXP + 1] : 0.0, S2 = kGrad ? m[kXP + 2] : 0.0;
 #pragma unroll
     for (int n = kXP; n >= 1; --n) {
-      if (n == P) {  // start Horner at the last kept term
-        S0 = m[n];
-        if (kGrad) {
-          S1 = m[n + 1];
-          S2 = m[n + 2];
-        }
-      }
-      if (n <= P) {
-        const double xn = x * (1.0 / n);
-        S0 = fma(xn, S0, m[n - 1]);
-        if (kGrad) {
-          S1 = fma(xn, S1, m[n]);
-          S2 = fma(xn, S2, m[n + 1]);
-        }
+      const double xn = x * (1.0 / n);
+      S0 = fma(xn, S0, m[n - 1]);
+      if (kGrad) {
+        S1 = fma(xn, S1, m[n]);
+        S2 = fma(xn, S2, m[n + 1]);
       }
     }
     const double Rf = exp2_16_arg<kMode>(-gamma * gamma * kLog2eT);  // row factor R_i
@@ -517,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
   __shared__ __align__(128) float2 s_kwbuf[kF32 ? 2 : 1][kF32 ? kBJ : 1];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ double s_red[kThreads / 32][kNM];
+  __shared__ unsigned char s_cls[kMaxItemTiles];
 
   const int tid = threadIdx.x;
   const Item it = P.items[blockIdx.x];
@@ -591,17 +580,30 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
   struct Unit {
     int J, cnt, type;
   };
+  // Tile classes of the item, once, in parallel: low nibble = the class for
+  // this launch's halves, high nibble = the full (both-halves) class.
+  const int ntl = it.te - it.tb;
+  for (int k = tid; k < ntl; k += kThreads) {
+    const int ta = tile_type_all(it.tb + k, bi, P);
+    s_cls[k] = static_cast<unsigned char>(restrict_type(ta, P.halves) | (ta << 4));
+  }
+  __syncthreads();
   auto unit_at = [&](int J) {
-    int ty = kSkip;
-    while (J < it.te && (ty = tile_type(J, bi, P)) == kSkip) ++J;
-    Unit u{J, J < it.te ? 1 : 0, ty};
+    int k = J - it.tb;
+    while (k < ntl && (s_cls[k] & 15) == kSkip) ++k;
+    if (k >= ntl) return Unit{it.te, 0, kSkip};
+    const int ty = s_cls[k] & 15;
+    Unit u{it.tb + k, 1, ty};
     // Grouping follows the full (both-halves) classification, so a
     // background-only workspace refresh sums exactly like a full launch and
-    // cached results stay bitwise identical to fresh ones.
-    if (ty == kTileBx && tile_type_all(J, bi, P) == kTileBx)
-      while (u.cnt < kSlots && J + u.cnt < it.te && tile_type_all(J + u.cnt, bi, P) == kTileBx &&
-             expansion_ok(bi, P.d.t[J * kBJ], P.d.t[(J + u.cnt + 1) * kBJ - 1], P.c))
-        ++u.cnt;
+    // cached results stay bitwise identical to fresh ones: the longest run
+    // of Bx tiles (<= kSlots) whose span still qualifies for the expansion.
+    if (ty == kTileBx && (s_cls[k] >> 4) == kTileBx) {
+      int cnt = 1;
+      while (cnt < kSlots && k + cnt < ntl && (s_cls[k + cnt] >> 4) == kTileBx) ++cnt;
+      while (cnt > 1 && !expansion_ok(bi, P.d.t[u.J * kBJ], P.d.t[(u.J + cnt) * kBJ - 1], P.c)) --cnt;
+      u.cnt = cnt;
+    }
     return u;
   };
 

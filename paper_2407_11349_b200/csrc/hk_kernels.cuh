@@ -17,6 +17,7 @@ namespace hk {
 struct Item {
   int rb, re, tb, te, slot, pos;
 };
+constexpr int kMaxItemTiles = 1024;  // te - tb (the pair kernel classifies them in shared memory)
 
 // Per-evaluation coefficients, all derived on the host in double exactly
 // once (HawkesParams accessors, types.hpp:105-109; coefficients,
