@@ -204,7 +204,7 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
     if (kVarying) mask |= 1u << sK;
     if (kVarying && kGrad) mask |= (1u << sZ);
   }
-  const bool f32 = kVarying && type != kTileB && type != kTileM;  // FP32 skip-test columns
+  const bool f32 = kVarying && type != kTileB;  // FP32 candidate-test columns
   mbar_expect_tx(bar, kBytes * __popc(mask) + (f32 ? kBJ * sizeof(float4) : 0u));
   if (f32) bulk_g2s(fbuf, P.d.fxy + j0, kBJ * sizeof(float4), bar);
   const double* src[kSlots] = {P.d.t, P.d.x, P.d.y, P.d.w, P.d.v, P.d.z, P.d.K,
@@ -455,41 +455,55 @@ __device__ __forceinline__ void bg_expansion(RowState<NR>& R, const double* __re
   }
 }
 
-// M tiles: the reference's exact value guards, per pair.
-template <int NR, bool kVarying, bool kGrad, int kMode>
+// M tiles: the reference's exact value guards, per pair, for the halves
+// this launch needs.  Density-scaled trigger: only the warp's candidate
+// columns (warp_candidates; a dropped column's spatial exponent alone is
+// beyond the flush threshold, so its term is an exact 0 for every row).
+template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr>
 __device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
-                                            const double* __restrict__ buf, const EvalCoef& c) {
+                                            const double* __restrict__ buf,
+                                            const float4* __restrict__ fbuf, const EvalCoef& c) {
   const double* __restrict__ st = buf + sT * kBJ;
   const double* __restrict__ sx = buf + sX * kBJ;
   const double* __restrict__ sy = buf + sY * kBJ;
   const double* __restrict__ sk = buf + sK * kBJ;
   const double* __restrict__ sq = buf + sAux * kBJ;
   const double Kb = c.Kb, Kq0 = c.Kq0, Kw = c.Kw;
+  for (int cc = 0; cc < kBJ; cc += 32) {
+    const unsigned cand = (kTr && kVarying) ? warp_candidates(R, fbuf, cc) : 0xffffffffu;
+    if (!kBg && cand == 0u) continue;
 #pragma unroll 1
-  for (int j = 0; j < kBJ; ++j) {
-    const int jg = j0 + j;
-    const double tj = st[j], xj = sx[j], yj = sy[j];
-    const double qj = kVarying ? sq[j] : 1.0;
-    const double Kj = kVarying ? sk[j] : Kq0;
+    for (int k = 0; k < 32; ++k) {
+      const int j = cc + k;
+      const int jg = j0 + j;
+      const double tj = st[j];
+      const bool tr_col = kTr && ((cand >> k) & 1u);  // warp-uniform
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      const double td = R.t[r] - tj;
-      const double td2 = td * td;
-      double b = exp2_16<kMode>(td2, Kb);
-      const bool bg_ok = (jg < R.lb[r] || jg >= R.ub[r]) && jg < n;  // t_j != t_i
-      b = bg_ok ? b : 0.0;
-      R.B[r] += b;
-      if (kGrad) R.B2[r] = fma(td2, b, R.B2[r]);
-      const bool tr_ok = jg < R.lb[r];  // t_j < t_i
-      const double dx = R.x[r] - xj, dy = R.y[r] - yj;
-      const double d2 = fma(dx, dx, dy * dy);
-      const double A = fma(d2, Kj, td * Kw);
-      const double e = exp2_16_arg<kMode>(A);
-      const double g = tr_ok ? (kVarying ? e * qj : e) : 0.0;
-      R.T[r] += g;
-      if (kGrad) {
-        R.Td[r] = fma(td, g, R.Td[r]);
-        R.Tq[r] = fma(kVarying ? qj * d2 : d2, g, R.Tq[r]);
+      for (int r = 0; r < NR; ++r) {
+        const double td = R.t[r] - tj;
+        if (kBg) {
+          const double td2 = td * td;
+          double b = exp2_16<kMode>(td2, Kb);
+          const bool bg_ok = (jg < R.lb[r] || jg >= R.ub[r]) && jg < n;  // t_j != t_i
+          b = bg_ok ? b : 0.0;
+          R.B[r] += b;
+          if (kGrad) R.B2[r] = fma(td2, b, R.B2[r]);
+        }
+        if (tr_col) {
+          const double qj = kVarying ? sq[j] : 1.0;
+          const double Kj = kVarying ? sk[j] : Kq0;
+          const bool tr_ok = jg < R.lb[r];  // t_j < t_i
+          const double dx = R.x[r] - sx[j], dy = R.y[r] - sy[j];
+          const double d2 = fma(dx, dx, dy * dy);
+          const double A = fma(d2, Kj, td * Kw);
+          const double e = exp2_16_arg<kMode>(A);
+          const double g = tr_ok ? (kVarying ? e * qj : e) : 0.0;
+          R.T[r] += g;
+          if (kGrad) {
+            R.Td[r] = fma(td, g, R.Td[r]);
+            R.Tq[r] = fma(kVarying ? qj * d2 : d2, g, R.Tq[r]);
+          }
+        }
       }
     }
   }
@@ -646,7 +660,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
         bg_expansion<NR, kGrad, kMode>(R, buf, cur.cnt * kBJ, bi, P.c, s_red);
         break;
       default:
-        tile_masked<NR, kVarying, kGrad, kMode>(R, cur.J * kBJ, P.d.n, buf, P.c);
+        if (P.halves == kHalfBg)
+          tile_masked<NR, kVarying, kGrad, kMode, true, false>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
+        else if (P.halves == kHalfTr)
+          tile_masked<NR, kVarying, kGrad, kMode, false, true>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
+        else
+          tile_masked<NR, kVarying, kGrad, kMode, true, true>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
         break;
     }
     __syncthreads();  // every warp is done with this stage before it is refilled
