@@ -602,33 +602,46 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     s_cls[k] = static_cast<unsigned char>(restrict_type(ta, P.halves) | (ta << 4));
   }
   __syncthreads();
-  auto unit_at = [&](int J) {
-    int k = J - it.tb;
+  // Unit sequence (warp-uniform state): runs of expansion tiles (full class
+  // Bx or BTx) become one background unit over up to kSlots tiles, followed
+  // by a trigger unit (T) for each of its BTx tiles.  The runs follow the
+  // full classification, so a background-only workspace refresh groups and
+  // sums exactly like a full launch and cached results stay bitwise
+  // identical to fresh ones.
+  int next_k = 0, pend = 0, pend_end = 0;
+  auto expansion_class = [](int t) { return t == kTileBx || t == kTileBTx; };
+  auto unit_next = [&]() {
+    while (pend < pend_end) {
+      const int k = pend++;
+      if ((s_cls[k] & 15) == kTileBTx) return Unit{it.tb + k, 1, kTileT};
+    }
+    int k = next_k;
     while (k < ntl && (s_cls[k] & 15) == kSkip) ++k;
     if (k >= ntl) return Unit{it.te, 0, kSkip};
     const int ty = s_cls[k] & 15;
-    Unit u{it.tb + k, 1, ty};
-    // Grouping follows the full (both-halves) classification, so a
-    // background-only workspace refresh sums exactly like a full launch and
-    // cached results stay bitwise identical to fresh ones: the longest run
-    // of Bx tiles (<= kSlots) whose span still qualifies for the expansion.
-    if (ty == kTileBx && (s_cls[k] >> 4) == kTileBx) {
+    if (expansion_class(ty)) {
+      // the longest run (<= kSlots) whose span still qualifies
       int cnt = 1;
-      while (cnt < kSlots && k + cnt < ntl && (s_cls[k + cnt] >> 4) == kTileBx) ++cnt;
-      while (cnt > 1 && !expansion_ok(bi, P.d.t[u.J * kBJ], P.d.t[(u.J + cnt) * kBJ - 1], P.c)) --cnt;
-      u.cnt = cnt;
+      while (cnt < kSlots && k + cnt < ntl && expansion_class(s_cls[k + cnt] >> 4)) ++cnt;
+      const int J = it.tb + k;
+      while (cnt > 1 && !expansion_ok(bi, P.d.t[J * kBJ], P.d.t[(J + cnt) * kBJ - 1], P.c)) --cnt;
+      next_k = k + cnt;
+      pend = k;
+      pend_end = k + cnt;
+      return Unit{J, cnt, kTileBx};
     }
-    return u;
+    next_k = k + 1;
+    return Unit{it.tb + k, 1, ty};
   };
 
-  Unit cur = unit_at(it.tb);
+  Unit cur = unit_next();
   int stage = 0;
   unsigned phases = 0u;  // bit s = parity of the next wait on stage s
   if (cur.cnt && tid == 0)
     issue_tile<kVarying, kGrad, kF32>(cur.type, cur.J, cur.cnt, s_buf[0], s_fbuf[0], s_kwbuf[0],
                                       &s_bar[0], P);
   while (cur.cnt) {
-    const Unit nxt = unit_at(cur.J + cur.cnt);
+    const Unit nxt = unit_next();
     if (nxt.cnt && tid == 0)
       issue_tile<kVarying, kGrad, kF32>(nxt.type, nxt.J, nxt.cnt, s_buf[stage ^ 1],
                                         s_fbuf[kUseF ? stage ^ 1 : 0], s_kwbuf[kF32 ? stage ^ 1 : 0],
@@ -638,9 +651,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     const double* buf = s_buf[stage];
     const float4* fbuf = s_fbuf[kUseF ? stage : 0];
     const float2* kwbuf = s_kwbuf[kF32 ? stage : 0];
-    if (kF32 && (cur.type == kTileBT || cur.type == kTileBTx || cur.type == kTileT)) {
+    if (kF32 && (cur.type == kTileBT || cur.type == kTileT)) {
       if (cur.type == kTileBT) tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, fbuf, P.c);
-      if (cur.type == kTileBTx) bg_expansion<NR, kGrad, kMode>(R, buf + sT * kBJ, kBJ, bi, P.c, s_red);
       tile_trig_f32<NR, kVarying, kMode>(R, buf + sT * kBJ, fbuf, kwbuf, P.c);
     } else switch (cur.type) {
       case kTileBT:
@@ -652,11 +664,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
       case kTileT:
         tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, fbuf, P.c);
         break;
-      case kTileBTx:
-        bg_expansion<NR, kGrad, kMode>(R, buf + sT * kBJ, kBJ, bi, P.c, s_red);
-        tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, fbuf, P.c);
-        break;
-      case kTileBx:
+      case kTileBx:  // a run of expansion tiles (their triggers follow as T units)
         bg_expansion<NR, kGrad, kMode>(R, buf, cur.cnt * kBJ, bi, P.c, s_red);
         break;
       default:
