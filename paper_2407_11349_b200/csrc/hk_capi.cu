@@ -202,6 +202,8 @@ struct hk_ctx {
     s.re = re;
     ck(cudaSetDevice(dev), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    hk::upload_exp2_table(s.stream);
+    ck(cudaGetLastError(), "exp table");
     s.t = dmalloc<double>(npad);
     s.x = dmalloc<double>(npad);
     s.y = dmalloc<double>(npad);

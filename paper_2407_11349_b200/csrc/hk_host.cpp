@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <numeric>
 
 #include "hk_device.cuh"
@@ -108,6 +109,19 @@ void benchmark_catalog(std::size_t n, std::uint64_t seed, double* t, double* x, 
     x[i] = xx[order[i]];
     y[i] = yy[order[i]];
     d[i] = dd[order[i]];
+  }
+}
+
+void make_exp2_table(double* out, int n) {
+  int b = 0;
+  while ((1 << b) < n) ++b;
+  for (int j = 0; j < n; ++j) {
+    // long double exp2 (64-bit significand), rounded once to double
+    const double v = static_cast<double>(std::exp2l(static_cast<long double>(j) / n));
+    std::uint64_t u;
+    std::memcpy(&u, &v, sizeof u);
+    u -= static_cast<std::uint64_t>(j) << (32 + 20 - b);  // high word minus (j << (20 - b))
+    std::memcpy(&out[j], &u, sizeof u);
   }
 }
 

@@ -916,10 +916,21 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* sink, int iters
 
 template <bool V, bool G, int M, bool F>
 void launch_pair_t(const PairParams& P, int n_items, cudaStream_t s) {
-  pair_kernel<V, G, M, F><<<n_items, kThreads, 0, s>>>(P);
+  constexpr int kTabBytes = kTab * static_cast<int>(sizeof(double));  // dynamic: the exp table
+  // static + dynamic exceed the default 48 KB: opt in (on the current device)
+  cudaFuncSetAttribute(pair_kernel<V, G, M, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kTabBytes);
+  pair_kernel<V, G, M, F><<<n_items, kThreads, kTabBytes, s>>>(P);
 }
 
 }  // namespace
+
+void upload_exp2_table(cudaStream_t s) {
+  double tab[kTab];
+  make_exp2_table(tab, kTab);
+  cudaMemcpyToSymbolAsync(g_exp2_tab, tab, sizeof(tab), 0, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+}
 
 void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
   const int threads = 256;

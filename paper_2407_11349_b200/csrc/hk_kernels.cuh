@@ -63,6 +63,11 @@ struct DeviceCatalog {
 // Row-sum halves: the background [B, B2] and the trigger [T, Td, Tq].
 constexpr int kHalfBg = 1, kHalfTr = 2;
 
+// The exp table (hk_device.cuh) of the current device; once per device
+// before the first pair launch.
+void upload_exp2_table(cudaStream_t s);
+// 2^(j/n), j < n, each high word minus (j << (20 - log2 n)) (host).
+void make_exp2_table(double* out, int n);
 void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
 // Spatially clusters the rows [rows_base, rows_base + rows) window by window
 // (window rows each, k-d median splits down to `leaf` rows) into rperm;
