@@ -65,8 +65,8 @@ int guarded(Fn&& fn) {
 // overrides; 1 disables the clustering).
 int row_window() {
   const char* e = std::getenv("HK_ROW_WINDOW");
-  const int w = e ? std::atoi(e) : 16;
-  return (w == 1 || w == 2 || w == 4 || w == 8 || w == 16) ? w : 16;
+  const int w = e ? std::atoi(e) : 32;
+  return (w == 1 || w == 2 || w == 4 || w == 8 || w == 16 || w == 32) ? w : 32;
 }
 
 template <typename T>

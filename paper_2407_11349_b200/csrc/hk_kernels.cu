@@ -737,7 +737,7 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
 // row clustering (varying kernel): one CTA per row window
 
 constexpr int kClusterThreads = 1024;
-constexpr int kMaxWindow = 4096;
+constexpr int kMaxWindow = 8192;
 
 // k-d median splits by sorting: the window is sorted by x, each half by y,
 // each quarter by x, ... down to `leaf` rows (one warp's rows).  Every
@@ -746,8 +746,11 @@ constexpr int kMaxWindow = 4096;
 __global__ void __launch_bounds__(kClusterThreads)
     cluster_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm,
                    int rows_base, int rows, int window, int leaf, double cx, double cy) {
-  __shared__ float kx[kMaxWindow], ky[kMaxWindow];
-  __shared__ int kv[kMaxWindow];
+  // dynamic shared memory (aliases the exp table of other kernels): window
+  // keys x, keys y, rows
+  float* kx = reinterpret_cast<float*>(s_exp2_tab);
+  float* ky = kx + window;
+  int* kv = reinterpret_cast<int*>(ky + window);
   const int w0 = blockIdx.x * window;
   for (int i = threadIdx.x; i < window; i += kClusterThreads) {
     const int li = w0 + i;
@@ -941,8 +944,10 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
                     int window, int leaf, double cx, double cy, cudaStream_t s) {
   if (rows <= 0 || window > kMaxWindow || window < leaf) return;
   const int windows = (rows + window - 1) / window;
-  cluster_kernel<<<windows, kClusterThreads, 0, s>>>(x, y, rperm, rows_base, rows, window, leaf, cx,
-                                                     cy);
+  const int bytes = window * 12;
+  cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cluster_kernel<<<windows, kClusterThreads, bytes, s>>>(x, y, rperm, rows_base, rows, window, leaf,
+                                                         cx, cy);
 }
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,

@@ -313,6 +313,36 @@ def test_bg_expansion_matches_direct(eng, variant):
     np.testing.assert_allclose(g_x, g_d, rtol=1e-12, atol=1e-12 * np.abs(g_d).max())
 
 
+def test_row_windows_agree(eng, oracle, monkeypatch):
+    """Density-scaled kernel: the spatially clustered row windows (default
+    32 row blocks, HK_ROW_WINDOW) only reorder rows and widen the masked
+    band, so windows of 1, 4 and 32 blocks agree to rounding, and each
+    matches the long-double oracle; a window is bitwise deterministic.
+    County-like catalog: densities log-uniform per 0.5-degree cell."""
+    t, x, y, _ = eng.benchmark_catalog(20000, 9).arrays()
+    rng = np.random.default_rng(3)
+    dens = np.exp(rng.uniform(0, np.log(7.4e4), 400))
+    cell = (np.minimum(np.floor((x + 5) / 0.5), 19) + 20 * np.minimum(np.floor((y + 5) / 0.5), 19)).astype(int)
+    cat = eng.Catalog(t, x, y, dens[cell])
+    p = dict(BENCH)
+    out = {}
+    for w in ("1", "4", "32"):
+        monkeypatch.setenv("HK_ROW_WINDOW", w)
+        ev = eng.Evaluator(cat)
+        a = ev.eval(hp(eng, p, 1), grad=True)
+        b = ev.eval(hp(eng, p, 1), grad=True)
+        assert a[0] == b[0] and np.array_equal(a[1], b[1])
+        out[w] = a
+        ev.close()
+    ll_o, g_o = oracle.ll_grad(cat.arrays(), p, 1)
+    _, scale = oracle.grad_scale(cat.arrays(), p, 1)
+    for w, (ll, g) in out.items():
+        assert abs(ll - out["1"][0]) <= 1e-13 * abs(ll), w
+        np.testing.assert_allclose(g, out["1"][1], rtol=1e-12, atol=1e-12 * np.abs(g).max())
+        assert abs(ll - ll_o) <= LL_TOL * abs(ll_o)
+        check_grad(g, g_o, scale)
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 def test_full_60k_vs_reference_and_oracle(eng, oracle, reference, variant):
     """N=6e4 (row blocks qualify for the background expansion): whole-catalog
