@@ -204,7 +204,7 @@ def run_ours(args):
     cat = benchmark_catalog(args.n, 42)
     p = HawkesParams(**BENCH_PARAMS, variant=Variant[args.variant])
     if use_dist:
-        sh = ShardedLikelihood(cat, device=local)
+        sh = ShardedLikelihood(cat, device=local, variant=p.variant)
         ev, stream = sh.ev, sh.stream
     else:
         sh = None

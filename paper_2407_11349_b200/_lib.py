@@ -64,6 +64,7 @@ SIGNATURES = [
     ("hk_validate_params", C.c_int, [_pp]),
     ("hk_partition_make", C.c_int, [_sz, _sz, _szp]),
     ("hk_plan_shards", C.c_int, [_dp, _sz, _sz, _szp]),
+    ("hk_plan_shards_variant", C.c_int, [_dp, _sz, _sz, C.c_int, _szp]),
     ("hk_benchmark_catalog", C.c_int, [_sz, C.c_uint64, _dp, _dp, _dp, _dp]),
     ("hk_measure_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("hk_last_error", C.c_char_p, []),

@@ -686,18 +686,25 @@ int hk_partition_make(size_t n, size_t g, size_t* bounds) {
   });
 }
 
-int hk_plan_shards(const double* t, size_t n, size_t g, size_t* bounds) {
+int hk_plan_shards_variant(const double* t, size_t n, size_t g, int variant, size_t* bounds) {
   return guarded([&] {
     if (!t || !bounds) throw std::invalid_argument("hk_plan_shards: null argument");
+    if (variant != HK_VARIANT_CONSTANT && variant != HK_VARIANT_VARYING)
+      throw std::invalid_argument("hk_plan_shards: unknown variant");
     std::vector<double> tv(t, t + n);
     for (size_t i = 1; i < n; ++i)
       if (tv[i - 1] > tv[i])
         throw std::invalid_argument("Catalog: times not sorted at index " + std::to_string(i));
     std::vector<int> lb, ub;
     hk::tie_bounds(tv, lb, ub);
-    const auto b = hk::plan_shards(lb, g);
+    const auto b = hk::plan_shards(lb, g,
+                                   variant == HK_VARIANT_VARYING ? hk::kCostBetaVarying : hk::kCostBeta);
     std::copy(b.begin(), b.end(), bounds);
   });
+}
+
+int hk_plan_shards(const double* t, size_t n, size_t g, size_t* bounds) {
+  return hk_plan_shards_variant(t, n, g, HK_VARIANT_CONSTANT, bounds);
 }
 
 int hk_benchmark_catalog(size_t n, uint64_t seed, double* t, double* lon, double* lat,

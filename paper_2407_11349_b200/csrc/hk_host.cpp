@@ -150,13 +150,13 @@ void tie_bounds(const std::vector<double>& t, std::vector<int>& lb, std::vector<
   }
 }
 
-std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g) {
+std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g, double beta) {
   const std::size_t n = lb.size();
   if (g == 0) throw std::invalid_argument("plan_shards: shard count must be positive");
   if (g > n) throw std::invalid_argument("plan_shards: more shards than rows");
   std::vector<double> cum(n + 1, 0.0);
   const double row_bg = background_cost(n) * static_cast<double>(n - 1);
-  for (std::size_t i = 0; i < n; ++i) cum[i + 1] = cum[i] + row_bg + kCostBeta * lb[i];
+  for (std::size_t i = 0; i < n; ++i) cum[i + 1] = cum[i] + row_bg + beta * lb[i];
   std::vector<std::size_t> b(g + 1, 0);
   b[g] = n;
   for (std::size_t s = 1; s < g; ++s) {

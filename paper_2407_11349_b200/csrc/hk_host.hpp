@@ -47,7 +47,12 @@ constexpr std::size_t kExpansionRows = 32768;  // catalogs at least this large e
 inline double background_cost(std::size_t n) {
   return n >= kExpansionRows ? kCostAlphaExpanded : kCostAlphaDirect;
 }
-std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g);
+// The density-scaled kernel culls its trigger spatially: per earlier row it
+// costs ~3.2 (fit of full(e) = a e + b e^2/2 to the LL+grad times of row
+// prefixes [0, e) at N=1e6: a = 23.8 ms, b = 76 ms, b/a = 3.2).
+constexpr double kCostBetaVarying = 3.2;
+std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g,
+                                     double beta = kCostBeta);
 
 // Work items for rows [rb, re) of an n-event catalog: row blocks of
 // rows_per_item rows times column chunks of whole tiles; heaviest first.  Returns the

@@ -551,7 +551,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     if (kVarying && it.pos >= 0) {
       row = P.d.rperm[it.pos + pos0 + r * kPosStride];
       valid[r] = row >= 0;
-      row = valid[r] ? row : it.rb;
+      // padding positions sit at the window's tail: borrow the warp's first
+      // row (or the window's first row for an all-padding warp)
+      if (!valid[r]) {
+        row = P.d.rperm[it.pos + (tid >> 5) * 32 * NR];
+        row = row >= 0 ? row : it.rb;
+      }
     } else {
       row = it.rb + pos0 + r * kPosStride;
       valid[r] = row < it.re;
@@ -567,9 +572,13 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     R.B[r] = R.B2[r] = R.T[r] = R.Td[r] = R.Tq[r] = 0.0;
   }
   if (kVarying) {
-    float x0 = R.xf[0], x1 = R.xf[0], y0 = R.yf[0], y1 = R.yf[0];
+    // the box of the warp's VALID rows (empty for an all-padding warp: no
+    // candidates); padding rows are computed but never stored
+    const float kInf = __int_as_float(0x7f800000);
+    float x0 = kInf, x1 = -kInf, y0 = kInf, y1 = -kInf;
 #pragma unroll
-    for (int r = 1; r < NR; ++r) {
+    for (int r = 0; r < NR; ++r) {
+      if (!valid[r]) continue;
       x0 = fminf(x0, R.xf[r]);
       x1 = fmaxf(x1, R.xf[r]);
       y0 = fminf(y0, R.yf[r]);

@@ -50,12 +50,13 @@ class ShardedLikelihood:
     C ABI.
     """
 
-    def __init__(self, catalog: Catalog, group=None, device: int | None = None, shard_eval=None):
+    def __init__(self, catalog: Catalog, group=None, device: int | None = None, shard_eval=None,
+                 variant=0):
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.catalog = catalog
-        self.bounds = plan_shards(catalog.t, self.world)
+        self.bounds = plan_shards(catalog.t, self.world, variant)
         b, e = int(self.bounds[self.rank]), int(self.bounds[self.rank + 1])
         self.rows = (b, e)
         self.on_gpu = shard_eval is None

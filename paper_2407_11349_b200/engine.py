@@ -145,11 +145,13 @@ def make_partition(n: int, g: int) -> Partition:
     return Partition.make(n, g)
 
 
-def plan_shards(t, g: int) -> np.ndarray:
-    """Cost-balanced row-shard boundaries (g+1) for g devices/ranks."""
+def plan_shards(t, g: int, variant: "Variant | int" = 0) -> np.ndarray:
+    """Cost-balanced row-shard boundaries (g+1) for g devices/ranks, for
+    the kernel variant the shards will mostly run (the density-scaled
+    kernel's trigger is spatially culled, so its rows weigh differently)."""
     t = _f64(t)
     b = np.zeros(g + 1, dtype=np.uintp)
-    check(lib.hk_plan_shards(t, len(t), g, b))
+    check(lib.hk_plan_shards_variant(t, len(t), g, int(variant), b))
     return b.astype(np.int64)
 
 

@@ -70,6 +70,13 @@ def test_plan_shards_balanced():
         cost = 1.0 * (len(t) - 1) + 16.0 * lb  # N >= 32768: expanded background
         w = np.array([cost[b[i]:b[i + 1]].sum() for i in range(g)])
         assert w.max() / w.mean() < 1.001
+    # the density-scaled kernel's culled trigger weighs 3.2 per earlier row
+    for g in (2, 8):
+        b = plan_shards(t, g, 1)
+        cost = 1.0 * (len(t) - 1) + 3.2 * lb
+        w = np.array([cost[b[i]:b[i + 1]].sum() for i in range(g)])
+        assert w.max() / w.mean() < 1.001
+        assert not np.array_equal(b, plan_shards(t, g, 0))
     # small catalogs (direct background) weigh the background at 13
     ts = benchmark_catalog(5000, 3).t
     lbs = np.searchsorted(ts, ts, side="left")

@@ -20,20 +20,28 @@ cat = benchmark_catalog(n, 42)
 p = HawkesParams(mu0=1.0, tau_t=5.0, xi0=0.5, sigma_x=0.5, sigma_t=2.0, area=100.0, variant=v)
 
 
-def shard_ms(b, e):
+def shard_ms(b, e, reps=5):
+    """Median pair-kernel time of `reps` evaluations of rows [b, e) after
+    one warm-up evaluation."""
     ev = Evaluator(cat, shard=(int(b), int(e)))
     ev.eval(p, grad=True)
-    ev.set_profiling(True)
-    ev.eval(p, grad=True)
-    ms, k, _ = ev.profile()
+    t = []
+    for _ in range(reps):
+        ev.reset_profile()
+        ev.set_profiling(True)
+        ev.eval(p, grad=True)
+        ms, k, _ = ev.profile()
+        ev.set_profiling(False)
+        t.append(ms / k)
     ev.close()
-    return ms / k
+    return float(np.median(t))
 
 
+shard_ms(0, n, reps=3)  # clocks up before anything is timed
 full = shard_ms(0, n)
 print(f"N={n} variant={v.name}: 1 GPU {full:.1f} ms")
 for g in (2, 4, 8):
-    bounds = plan_shards(cat.t, g)
+    bounds = plan_shards(cat.t, g, v)
     ms = np.array([shard_ms(bounds[k], bounds[k + 1]) for k in range(g)])
     print(f"g={g}: shard ms {np.round(ms, 1).tolist()}  max/mean {ms.max() / ms.mean():.3f}  "
           f"sum {ms.sum():.1f} ms ({ms.sum() / full:.3f} of 1 GPU)  projected {g}-GPU {ms.max():.1f} ms "
