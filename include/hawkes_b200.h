@@ -165,8 +165,9 @@ int hk_partition_make(size_t n, size_t g, size_t* bounds);
 
 /* Cost-balanced contiguous row shards for g devices: boundaries (g+1) such
  * that each shard carries ~1/g of the pair work, row n costing
- * alpha*(N-1) + 16*count_before(t_n) FP64 instructions, alpha = 1 for
- * N >= 32768 (background block expansion) and 13 below (direct). */
+ * alpha*(N-1) + beta*count_before(t_n): alpha = 13, beta = 16 (FP64 per pair)
+ * on the direct path, alpha = 1, beta = 46 (measured) for N >= 32768 where
+ * the background block expansion applies. */
 int hk_plan_shards(const double* t, size_t n, size_t g, size_t* bounds);
 
 /* The same for the kernel variant the shards will mostly run: the

@@ -423,7 +423,9 @@ int hk_create(const double* t, const double* lon, const double* lat, const doubl
       throw std::invalid_argument("hk_create: requested " + std::to_string(g) +
                                   " GPUs, " + std::to_string(avail) + " visible");
     if (static_cast<std::size_t>(g) > n) throw std::invalid_argument("Partition: more workers than terms");
-    const auto bounds = hk::plan_shards(ctx->lb, static_cast<std::size_t>(g));
+    const auto bounds = hk::plan_shards(
+        ctx->lb, static_cast<std::size_t>(g),
+        n >= hk::kExpansionRows ? hk::kCostBetaExpanded : hk::kCostBeta);
     ctx->devs.resize(g);
     for (int i = 0; i < g; ++i)
       ctx->init_device(ctx->devs[i], i, static_cast<int>(bounds[i]), static_cast<int>(bounds[i + 1]));
@@ -697,8 +699,10 @@ int hk_plan_shards_variant(const double* t, size_t n, size_t g, int variant, siz
         throw std::invalid_argument("Catalog: times not sorted at index " + std::to_string(i));
     std::vector<int> lb, ub;
     hk::tie_bounds(tv, lb, ub);
-    const auto b = hk::plan_shards(lb, g,
-                                   variant == HK_VARIANT_VARYING ? hk::kCostBetaVarying : hk::kCostBeta);
+    const double beta = variant == HK_VARIANT_VARYING ? hk::kCostBetaVarying
+                        : n >= hk::kExpansionRows        ? hk::kCostBetaExpanded
+                                                         : hk::kCostBeta;
+    const auto b = hk::plan_shards(lb, g, beta);
     std::copy(b.begin(), b.end(), bounds);
   });
 }

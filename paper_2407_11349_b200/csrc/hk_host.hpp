@@ -42,7 +42,12 @@ void tie_bounds(const std::vector<double>& t, std::vector<int>& lb, std::vector<
 // alpha = background_cost(n) picks between the two.
 constexpr double kCostAlphaDirect = 13.0;    // FP64 per background pair, direct
 constexpr double kCostAlphaExpanded = 1.0;   // ... with the block expansion (rounded up)
-constexpr double kCostBeta = 16.0;           // FP64 per trigger pair
+constexpr double kCostBeta = 16.0;           // FP64 per trigger pair (direct background)
+// With the background expanded, the measured per-row cost of the homogeneous
+// kernel is a + b t_n/T with b/a = 46 (fit of sixteen 1/16 row ranges at
+// N=1e6: 3.32 + 3.93 k ms): the trigger weighs 46 against 1 per background
+// column.
+constexpr double kCostBetaExpanded = 46.0;
 constexpr std::size_t kExpansionRows = 32768;  // catalogs at least this large expand
 inline double background_cost(std::size_t n) {
   return n >= kExpansionRows ? kCostAlphaExpanded : kCostAlphaDirect;

@@ -67,7 +67,7 @@ def test_plan_shards_balanced():
     for g in (1, 2, 4, 8):
         b = plan_shards(t, g)
         assert b[0] == 0 and b[-1] == len(t) and np.all(np.diff(b) > 0)
-        cost = 1.0 * (len(t) - 1) + 16.0 * lb  # N >= 32768: expanded background
+        cost = 1.0 * (len(t) - 1) + 46.0 * lb  # N >= 32768: expanded background
         w = np.array([cost[b[i]:b[i + 1]].sum() for i in range(g)])
         assert w.max() / w.mean() < 1.001
     # the density-scaled kernel's culled trigger weighs 3.2 per earlier row
