@@ -14,6 +14,11 @@ all: $(LIB) oracle
 $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared $(SRCS) -o $@ 2> build_ptxas.log || (cat build_ptxas.log; false)
 
+# Device bounds checks (HK_ASSERT) on: run the GPU tests against it with
+# HK_LIB=paper_2407_11349_b200/libhawkes_b200_debug.so.
+debug: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -DHK_DEBUG -shared $(SRCS) -o paper_2407_11349_b200/libhawkes_b200_debug.so 2> build_ptxas_debug.log || (cat build_ptxas_debug.log; false)
+
 oracle:
 	$(MAKE) -C oracle
 
@@ -21,7 +26,7 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -f $(LIB) build_ptxas.log
+	rm -f $(LIB) paper_2407_11349_b200/libhawkes_b200_debug.so build_ptxas.log build_ptxas_debug.log
 	$(MAKE) -C oracle clean
 
-.PHONY: all oracle ref clean
+.PHONY: all oracle ref clean debug

@@ -38,6 +38,7 @@
 //   skip tiles whose every term flushes to zero in this arithmetic.
 #include <cuda_runtime.h>
 
+#include <cassert>
 #include <cstdint>
 
 #include "hk_device.cuh"
@@ -46,6 +47,14 @@
 namespace hk {
 
 namespace {
+
+// Device-side bounds checks of the debug build (make debug: -DHK_DEBUG);
+// compiled out otherwise.
+#ifdef HK_DEBUG
+#define HK_ASSERT(x) assert(x)
+#else
+#define HK_ASSERT(x) ((void)0)
+#endif
 
 enum TileType { kSkip = 0, kTileBT = 1, kTileB = 2, kTileT = 3, kTileM = 4, kTileBTx = 5, kTileBx = 6 };
 
@@ -178,6 +187,8 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
                                            float2* kwbuf, uint64_t* bar, const PairParams& P) {
   const int j0 = J * kBJ;
   constexpr unsigned kBytes = kBJ * sizeof(double);
+  HK_ASSERT(J >= 0 && cnt >= 1 && cnt <= kSlots && (J + cnt) * kBJ <= P.d.npad);
+  HK_ASSERT(type == kTileBx || cnt == 1);
   if (type == kTileBx) {  // a group of cnt background-only tiles: their times, contiguous
     mbar_expect_tx(bar, kBytes * cnt);
     bulk_g2s(buf, P.d.t + j0, kBytes * cnt, bar);
@@ -606,6 +617,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
   // Tile classes of the item, once, in parallel: low nibble = the class for
   // this launch's halves, high nibble = the full (both-halves) class.
   const int ntl = it.te - it.tb;
+  HK_ASSERT(ntl >= 0 && ntl <= kMaxItemTiles && it.te * kBJ <= P.d.npad);
   for (int k = tid; k < ntl; k += kThreads) {
     const int ta = tile_type_all(it.tb + k, bi, P);
     s_cls[k] = static_cast<unsigned char>(restrict_type(ta, P.halves) | (ta << 4));
@@ -697,6 +709,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     if (!valid[r]) continue;
     const int row = (kVarying && it.pos >= 0) ? P.d.rperm[it.pos + pos0 + r * kPosStride]
                                               : it.rb + pos0 + r * kPosStride;
+    HK_ASSERT(row >= P.rows_base && row < P.rows_base + P.rows_total);
+    HK_ASSERT(row >= it.rb && row < it.re);  // the item's own block / window
     const size_t i = static_cast<size_t>(row - P.rows_base);
     out[0 * plane + i] = R.B[r];
     out[1 * plane + i] = R.B2[r];
@@ -761,6 +775,7 @@ __global__ void __launch_bounds__(kClusterThreads)
   float* ky = kx + window;
   int* kv = reinterpret_cast<int*>(ky + window);
   const int w0 = blockIdx.x * window;
+  HK_ASSERT(window <= kMaxWindow && window % leaf == 0 && blockDim.x == kClusterThreads);
   for (int i = threadIdx.x; i < window; i += kClusterThreads) {
     const int li = w0 + i;
     const bool ok = li < rows;
