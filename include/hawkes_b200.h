@@ -78,6 +78,12 @@ typedef struct hk_ctx hk_ctx;
 int hk_create(const double* t, const double* lon, const double* lat, const double* density,
               size_t n, int n_gpus, hk_ctx** out);
 
+/* hk_create whose multi-device shard plan is balanced for `variant` (the
+ * kernel the caller mostly runs; see hk_plan_shards_variant).  Evaluations
+ * may still use either variant. */
+int hk_create_variant(const double* t, const double* lon, const double* lat, const double* density,
+                      size_t n, int n_gpus, int variant, hk_ctx** out);
+
 /* One rank's shard for a one-process-per-GPU job: the full catalog is
  * uploaded to `device`, but only rows [row_begin, row_end) are evaluated.
  * hk_eval then returns this shard's partial sums; the caller reduces the

@@ -58,10 +58,12 @@ inline hk_params to_c(const HawkesParams& p, Variant v) {
 
 }  // namespace detail
 
-/// One engine context: the catalog resident on `n_gpus` devices.
+/// One engine context: the catalog resident on `n_gpus` devices, sharded
+/// for the kernel variant `plan_for` (evaluations may use either).
 class Engine {
  public:
-  explicit Engine(const Catalog& catalog, int n_gpus = 1) : ctx_(nullptr, &hk_destroy) {
+  explicit Engine(const Catalog& catalog, int n_gpus = 1, Variant plan_for = Variant::constant)
+      : ctx_(nullptr, &hk_destroy) {
     const std::size_t n = catalog.size();
     std::vector<double> t(n), x(n), y(n), d(n);
     for (std::size_t i = 0; i < n; ++i) {
@@ -71,7 +73,10 @@ class Engine {
       d[i] = catalog[i].density;
     }
     hk_ctx* raw = nullptr;
-    detail::check(hk_create(t.data(), x.data(), y.data(), d.data(), n, n_gpus, &raw));
+    detail::check(hk_create_variant(t.data(), x.data(), y.data(), d.data(), n, n_gpus,
+                                    plan_for == Variant::varying ? HK_VARIANT_VARYING
+                                                                 : HK_VARIANT_CONSTANT,
+                                    &raw));
     ctx_.reset(raw);
   }
 

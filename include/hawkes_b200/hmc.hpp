@@ -69,7 +69,7 @@ class HmcSampler {
       : cfg_(config),
         catalog_(&catalog),
         regions_(regions),
-        engine_(catalog, config.n_gpus),
+        engine_(catalog, config.n_gpus, config.chain.initial.variant),
         location_rng_(config.chain.seed),
         param_rng_(config.chain.seed ^ 0x9e3779b97f4a7c15ull) {
     cfg_.chain.validate();

@@ -43,6 +43,7 @@ _pp = C.POINTER(hk_params)
 # (name, restype, argtypes) for every symbol declared in include/hawkes_b200.h
 SIGNATURES = [
     ("hk_create", C.c_int, [_dp, _dp, _dp, _dp, _sz, C.c_int, C.POINTER(_ctx)]),
+    ("hk_create_variant", C.c_int, [_dp, _dp, _dp, _dp, _sz, C.c_int, C.c_int, C.POINTER(_ctx)]),
     ("hk_create_shard", C.c_int, [_dp, _dp, _dp, _dp, _sz, _sz, _sz, C.c_int, C.POINTER(_ctx)]),
     ("hk_destroy", None, [_ctx]),
     ("hk_set_locations", C.c_int, [_ctx, _dp, _dp]),

@@ -412,8 +412,15 @@ const char* hk_version(void) { return "hawkes_b200 0.1 (sm_100a)"; }
 
 int hk_create(const double* t, const double* lon, const double* lat, const double* density,
               size_t n, int n_gpus, hk_ctx** out) {
+  return hk_create_variant(t, lon, lat, density, n, n_gpus, HK_VARIANT_CONSTANT, out);
+}
+
+int hk_create_variant(const double* t, const double* lon, const double* lat, const double* density,
+                      size_t n, int n_gpus, int variant, hk_ctx** out) {
   return guarded([&] {
     if (!out) throw std::invalid_argument("hk_create: null output");
+    if (variant != HK_VARIANT_CONSTANT && variant != HK_VARIANT_VARYING)
+      throw std::invalid_argument("hk_create: unknown variant");
     *out = nullptr;
     auto ctx = new_ctx(t, lon, lat, density, n);
     int avail = 0;
@@ -423,9 +430,10 @@ int hk_create(const double* t, const double* lon, const double* lat, const doubl
       throw std::invalid_argument("hk_create: requested " + std::to_string(g) +
                                   " GPUs, " + std::to_string(avail) + " visible");
     if (static_cast<std::size_t>(g) > n) throw std::invalid_argument("Partition: more workers than terms");
-    const auto bounds = hk::plan_shards(
-        ctx->lb, static_cast<std::size_t>(g),
-        n >= hk::kExpansionRows ? hk::kCostBetaExpanded : hk::kCostBeta);
+    const double beta = variant == HK_VARIANT_VARYING ? hk::kCostBetaVarying
+                        : n >= hk::kExpansionRows        ? hk::kCostBetaExpanded
+                                                         : hk::kCostBeta;
+    const auto bounds = hk::plan_shards(ctx->lb, static_cast<std::size_t>(g), beta);
     ctx->devs.resize(g);
     for (int i = 0; i < g; ++i)
       ctx->init_device(ctx->devs[i], i, static_cast<int>(bounds[i]), static_cast<int>(bounds[i + 1]));
