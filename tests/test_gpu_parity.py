@@ -343,6 +343,41 @@ def test_row_windows_agree(eng, oracle, monkeypatch):
         check_grad(g, g_o, scale)
 
 
+@pytest.mark.parametrize("sigma_x,dens_max,origin", [
+    (0.5, 1e8, (0.0, 0.0)),        # radii down to ~2e-3 degrees
+    (0.02, 1e4, (-120.0, 36.0)),   # tiny lengthscale, far from the origin
+    (3.0, 10.0, (150.0, -33.0)),   # every column wide
+], ids=["extreme-density", "tiny-sigma-offset", "wide"])
+def test_culling_regimes_vs_oracle(eng, oracle, sigma_x, dens_max, origin):
+    """Density-scaled trigger culling (clustered rows, FP32 box test with the
+    rounded-up thresholds): clustered catalogs (events in 40 hot spots) whose
+    per-source reach spans 3+ orders of magnitude, against the long-double
+    oracle, plus the window-1 (unclustered) path on the same catalog."""
+    rng = np.random.default_rng(11)
+    n = 12000
+    t = np.sort(rng.uniform(0, 100, n))
+    centres = rng.uniform(-5, 5, (40, 2))
+    k = rng.integers(0, 40, n)
+    x = origin[0] + centres[k, 0] + rng.normal(0, 0.3, n)
+    y = origin[1] + centres[k, 1] + rng.normal(0, 0.3, n)
+    d = np.exp(rng.uniform(0, np.log(dens_max), n))
+    cat = eng.Catalog(t, x, y, d)
+    p = dict(BENCH, sigma_x=sigma_x)
+    ll, g = eng.Evaluator(cat).eval(hp(eng, p, 1), grad=True)
+    ll_o, g_o = oracle.ll_grad(cat.arrays(), p, 1)
+    assert abs(ll - ll_o) <= LL_TOL * abs(ll_o), (ll, ll_o)
+    _, scale = oracle.grad_scale(cat.arrays(), p, 1)
+    check_grad(g, g_o, scale)
+    import os
+    os.environ["HK_ROW_WINDOW"] = "1"
+    try:
+        ll1, g1 = eng.Evaluator(cat).eval(hp(eng, p, 1), grad=True)
+    finally:
+        del os.environ["HK_ROW_WINDOW"]
+    assert abs(ll1 - ll) <= 1e-13 * abs(ll)
+    np.testing.assert_allclose(g1, g, rtol=1e-12, atol=1e-12 * np.abs(g).max())
+
+
 @pytest.mark.parametrize("variant", [0, 1])
 def test_full_60k_vs_reference_and_oracle(eng, oracle, reference, variant):
     """N=6e4 (row blocks qualify for the background expansion): whole-catalog
