@@ -712,11 +712,15 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     HK_ASSERT(row >= P.rows_base && row < P.rows_base + P.rows_total);
     HK_ASSERT(row >= it.rb && row < it.re);  // the item's own block / window
     const size_t i = static_cast<size_t>(row - P.rows_base);
-    out[0 * plane + i] = R.B[r];
-    out[1 * plane + i] = R.B2[r];
-    out[2 * plane + i] = R.T[r];
-    out[3 * plane + i] = R.Td[r];
-    out[4 * plane + i] = R.Tq[r];
+    if (P.halves & kHalfBg) {  // only this launch's half (split plans share the buffer)
+      out[0 * plane + i] = R.B[r];
+      out[1 * plane + i] = R.B2[r];
+    }
+    if (P.halves & kHalfTr) {
+      out[2 * plane + i] = R.T[r];
+      out[3 * plane + i] = R.Td[r];
+      out[4 * plane + i] = R.Tq[r];
+    }
   }
 }
 
