@@ -61,12 +61,19 @@ int guarded(Fn&& fn) {
   }
 }
 
-// Row blocks per clustering window of the varying plan (HK_ROW_WINDOW
-// overrides; 1 disables the clustering).
-int row_window() {
-  const char* e = std::getenv("HK_ROW_WINDOW");
-  const int w = e ? std::atoi(e) : 32;
-  return (w == 1 || w == 2 || w == 4 || w == 8 || w == 16 || w == 32) ? w : 32;
+// Row blocks per clustering window of the varying plan: the largest power
+// of two <= min(64, catalog blocks / 24) (measured: 64 at N=1e6, 16 at
+// N=1e5);
+// HK_ROW_WINDOW overrides (1 disables the clustering).
+int row_window(int rows) {
+  if (const char* e = std::getenv("HK_ROW_WINDOW")) {
+    const int w = std::atoi(e);
+    if (w == 1 || w == 2 || w == 4 || w == 8 || w == 16 || w == 32 || w == 64) return w;
+  }
+  const int blocks = (rows + hk::rows_per_item(true) - 1) / hk::rows_per_item(true);
+  int w = 1;
+  while (w < 64 && 2 * w * 24 <= blocks) w *= 2;
+  return w;
 }
 
 template <typename T>
@@ -227,7 +234,8 @@ struct hk_ctx {
     ck(cudaMemcpy(s.ub, ub.data(), n * sizeof(int), cudaMemcpyHostToDevice), "upload ub");
     // The varying kernel reads its rows in spatially clustered windows of
     // kRowWindow row blocks so that warps can skip columns (launch_cluster).
-    s.window = row_window();
+    // sized by the catalog (the trigger sweeps all n columns), not the shard
+    s.window = row_window(n);
     if (s.window > 1) {
       const int wr = s.window * hk::rows_per_item(true);
       s.rperm = dmalloc<int>(static_cast<std::size_t>((re - rb + wr - 1) / wr) * wr);

@@ -764,7 +764,7 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
 // row clustering (varying kernel): one CTA per row window
 
 constexpr int kClusterThreads = 1024;
-constexpr int kMaxWindow = 8192;
+constexpr int kMaxWindow = 16384;
 
 // k-d median splits by sorting: the window is sorted by x, each half by y,
 // each quarter by x, ... down to `leaf` rows (one warp's rows).  Every
