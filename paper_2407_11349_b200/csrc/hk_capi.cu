@@ -98,10 +98,10 @@ struct DeviceState {
   int window = 1;
   long rperm_loc = -1;
   // work plans per variant (rows per item differ, hk_device.cuh)
-  // plans: [0] constant, [1] varying (clustered windows), [2] the varying
-  // kernel's background half on contiguous row blocks (see enqueue)
-  hk::Item* items[3] = {nullptr, nullptr, nullptr};
-  int n_items[3] = {0, 0, 0}, slots[3] = {0, 0, 0};
+  // plans: [0] constant (also every background-only launch of the varying
+  // variant, see enqueue), [1] varying (clustered windows)
+  hk::Item* items[2] = {nullptr, nullptr};
+  int n_items[2] = {0, 0}, slots[2] = {0, 0};
   double* partial = nullptr;
   double* bg_sums[2] = {nullptr, nullptr};  // [B, B2] x rows, LRU-2 (workspace cache)
   double* tr_sums[2] = {nullptr, nullptr};  // [T, Td, Tq] x rows
@@ -240,7 +240,7 @@ struct hk_ctx {
       const int wr = s.window * hk::rows_per_item(true);
       s.rperm = dmalloc<int>(static_cast<std::size_t>((re - rb + wr - 1) / wr) * wr);
     }
-    for (int v = 0; v < 3; ++v) {
+    for (int v = 0; v < 2; ++v) {
       std::vector<hk::Item> items;
       s.slots[v] = hk::plan_items(lb, ub, n, rb, re, hk::rows_per_item(v != 0), items,
                                   v == 1 ? s.window : 1);
@@ -251,8 +251,7 @@ struct hk_ctx {
          "upload items");
     }
     const std::size_t rows = static_cast<std::size_t>(re - rb);
-    s.partial = dmalloc<double>(
-        static_cast<std::size_t>(std::max({s.slots[0], s.slots[1], s.slots[2]})) * 5 * rows);
+    s.partial = dmalloc<double>(static_cast<std::size_t>(std::max(s.slots[0], s.slots[1])) * 5 * rows);
     for (int k = 0; k < 2; ++k) {
       s.bg_sums[k] = dmalloc<double>(2 * rows);
       s.tr_sums[k] = dmalloc<double>(3 * rows);
@@ -355,15 +354,18 @@ struct hk_ctx {
       const int v = c.varying ? 1 : 0;
       // The density-scaled kernel's rows come in clustered windows that span
       // far more time than a row block, which would disqualify the
-      // background block expansion; its background half therefore runs as its
-      // own launch on contiguous row blocks (plan 2).  Full evaluations and
-      // background-only refreshes both take it from there, so cached and
-      // fresh sums stay bitwise identical.  Each launch writes only its
+      // background block expansion.  The background does not depend on the
+      // variant, so it runs as its own launch of the homogeneous kernel on
+      // the homogeneous plan: bitwise the background of a homogeneous
+      // evaluation, for full evaluations and background-only refreshes
+      // alike (the cache is keyed by tau alone).  Each launch writes only its
       // half's planes of the partial buffer.
       const bool split = c.varying && s.window > 1;
       if (split) {
+        hk::EvalCoef cb = c;
+        cb.varying = 0;
         if (halves & hk::kHalfBg)
-          hk::launch_pair(dc, c, s.items[2], s.n_items[2], s.partial, s.rb, rows, grad, hk::kHalfBg,
+          hk::launch_pair(dc, cb, s.items[0], s.n_items[0], s.partial, s.rb, rows, grad, hk::kHalfBg,
                           s.stream);
         if (halves & hk::kHalfTr)
           hk::launch_pair(dc, c, s.items[1], s.n_items[1], s.partial, s.rb, rows, grad, hk::kHalfTr,
@@ -374,7 +376,7 @@ struct hk_ctx {
       if (profiling) ck(cudaEventRecord(ev.second, s.stream), "cudaEventRecord");
       if (split) {
         if (halves & hk::kHalfBg)
-          hk::launch_collapse(s.partial, s.slots[2], rows, s.bg_sums[bgi], nullptr, s.stream);
+          hk::launch_collapse(s.partial, s.slots[0], rows, s.bg_sums[bgi], nullptr, s.stream);
         if (halves & hk::kHalfTr)
           hk::launch_collapse(s.partial, s.slots[1], rows, nullptr, s.tr_sums[tri], s.stream);
         prof_total += (halves == (hk::kHalfBg | hk::kHalfTr)) ? 5 : 3;

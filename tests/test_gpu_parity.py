@@ -425,6 +425,22 @@ def test_workspace_cache_bitwise_and_reuse(eng, variant):
     assert a[0] == b[0] and np.array_equal(a[1], b[1])
 
 
+def test_workspace_background_shared_across_variants(eng):
+    """The background half depends on tau alone and both variants compute it
+    with the same launch and plan, so a background cached by a homogeneous
+    evaluation serves a density-scaled one bitwise."""
+    cat = eng.benchmark_catalog(50000, 8)
+    pc, pv = hp(eng, BENCH, 0), hp(eng, BENCH, 1)
+    ev = eng.Evaluator(cat)
+    ev.ws_eval(pc, grad=True)
+    a = ev.ws_eval(pv, grad=True)  # background cached, trigger recomputed
+    b = eng.Evaluator(cat).eval(pv, grad=True)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1])
+    c = eng.Evaluator(cat).eval(pc, grad=True)
+    d = ev.ws_eval(pc, grad=True)
+    assert c[0] == d[0] and np.array_equal(c[1], d[1])
+
+
 def test_workspace_golden_script_cached(eng):
     """The reference workspace script (test_engine.cpp:159-190) through the
     cached workspace."""
