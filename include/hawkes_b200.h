@@ -178,7 +178,7 @@ int hk_plan_shards(const double* t, size_t n, size_t g, size_t* bounds);
 
 /* The same for the kernel variant the shards will mostly run: the
  * density-scaled (HK_VARIANT_VARYING) kernel culls its trigger spatially, so
- * its rows cost alpha*(N-1) + 3.2*count_before(t_n). */
+ * its rows cost alpha*(N-1) + 4.3*count_before(t_n). */
 int hk_plan_shards_variant(const double* t, size_t n, size_t g, int variant, size_t* bounds);
 
 /* benchmark_catalog(n, seed) (engine.hpp:251-259): the reference's

@@ -238,7 +238,8 @@ struct hk_ctx {
     s.window = row_window(n);
     if (s.window > 1) {
       const int wr = s.window * hk::rows_per_item(true);
-      s.rperm = dmalloc<int>(static_cast<std::size_t>((re - rb + wr - 1) / wr) * wr);
+      const int nb = (re - rb + hk::rows_per_item(true) - 1) / hk::rows_per_item(true);
+      s.rperm = dmalloc<int>(static_cast<std::size_t>(hk::window_count(nb, s.window)) * wr);
     }
     for (int v = 0; v < 2; ++v) {
       std::vector<hk::Item> items;
@@ -339,7 +340,9 @@ struct hk_ctx {
     const hk::DeviceCatalog dc = s.catalog(n, npad);
     const int rows = s.re - s.rb;
     if (c.varying && s.window > 1 && s.rperm_loc != loc_version) {
-      hk::launch_cluster(s.x, s.y, s.rperm, s.rb, rows, s.window * hk::rows_per_item(true),
+      const int bi = hk::rows_per_item(true);
+      hk::launch_cluster(s.x, s.y, s.rperm, s.rb, rows, s.window * bi,
+                         hk::window_count((rows + bi - 1) / bi, s.window),
                          32 * hk::rows_per_thread(true), c.cx, c.cy, s.stream);
       s.rperm_loc = loc_version;
       prof_total += 1;

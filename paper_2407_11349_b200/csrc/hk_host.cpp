@@ -195,9 +195,13 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
     // the block's own rows [r0, r1) and the rows [w0, w1) it is classified
     // against (its window)
     const int r0 = rb + b * kBI, r1 = std::min(re, r0 + kBI);
-    const int w0 = G > 1 ? rb + (b / G) * G * kBI : r0;
-    const int w1 = G > 1 ? std::min(re, w0 + G * kBI) : r1;
-    const int pos = G > 1 ? r0 - rb : -1;
+    // near-equal windows of <= G blocks; rperm holds G*kBI slots per window
+    const int nw = window_count(nblocks, G);
+    const int w = window_of_block(b, nblocks, nw);
+    const int b0 = window_first_block(w, nblocks, nw);
+    const int w0 = G > 1 ? rb + b0 * kBI : r0;
+    const int w1 = G > 1 ? std::min(re, rb + window_first_block(w + 1, nblocks, nw) * kBI) : r1;
+    const int pos = G > 1 ? w * G * kBI + (b - b0) * kBI : -1;
     const int lbmin = lb[w0], ubmax = ub[w1 - 1];
     for (int c = 0; c < slots; ++c) {
       const int tb = c * per, te = std::min(ntiles, (c + 1) * per);

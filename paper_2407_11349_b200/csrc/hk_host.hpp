@@ -53,9 +53,9 @@ inline double background_cost(std::size_t n) {
   return n >= kExpansionRows ? kCostAlphaExpanded : kCostAlphaDirect;
 }
 // The density-scaled kernel culls its trigger spatially: per earlier row it
-// costs ~3.2 (fit of full(e) = a e + b e^2/2 to the LL+grad times of row
-// prefixes [0, e) at N=1e6: a = 23.8 ms, b = 76 ms, b/a = 3.2).
-constexpr double kCostBetaVarying = 3.2;
+// costs ~4.3 (least-squares fit of full(e) = a e + b e^2/2 to the LL+grad
+// times of row prefixes [0, e) at N=1e6: a = 15.6 ms, b = 67.6 ms).
+constexpr double kCostBetaVarying = 4.3;
 std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g,
                                      double beta = kCostBeta);
 

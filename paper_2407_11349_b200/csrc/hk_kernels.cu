@@ -772,17 +772,25 @@ constexpr int kMaxWindow = 16384;
 // at the window's tail at every level.
 __global__ void __launch_bounds__(kClusterThreads)
     cluster_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm,
-                   int rows_base, int rows, int window, int leaf, double cx, double cy) {
+                   int rows_base, int rows, int window, int n_windows, int leaf, double cx,
+                   double cy) {
   // dynamic shared memory (aliases the exp table of other kernels): window
   // keys x, keys y, rows
   float* kx = reinterpret_cast<float*>(s_exp2_tab);
   float* ky = kx + window;
   int* kv = reinterpret_cast<int*>(ky + window);
-  const int w0 = blockIdx.x * window;
-  HK_ASSERT(window <= kMaxWindow && window % leaf == 0 && blockDim.x == kClusterThreads);
+  // window blockIdx.x: rows [w0, w1) of the shard, sorted into rperm slots
+  // [blockIdx.x * window, + window)
+  constexpr int kBI = kThreads * rows_per_thread(true);
+  const int nblocks = (rows + kBI - 1) / kBI;
+  const int w0 = window_first_block(blockIdx.x, nblocks, n_windows) * kBI;
+  const int w1 = min(rows, window_first_block(blockIdx.x + 1, nblocks, n_windows) * kBI);
+  const int window_rows = w1 - w0;
+  HK_ASSERT(window <= kMaxWindow && window % leaf == 0 && window_rows <= window &&
+            blockDim.x == kClusterThreads);
   for (int i = threadIdx.x; i < window; i += kClusterThreads) {
     const int li = w0 + i;
-    const bool ok = li < rows;
+    const bool ok = i < window_rows && li < rows;
     kx[i] = ok ? __double2float_rn(x[rows_base + li] - cx) : __int_as_float(0x7f800000);
     ky[i] = ok ? __double2float_rn(y[rows_base + li] - cy) : __int_as_float(0x7f800000);
     kv[i] = ok ? rows_base + li : -1;
@@ -813,7 +821,7 @@ __global__ void __launch_bounds__(kClusterThreads)
       }
     }
   }
-  for (int i = threadIdx.x; i < window; i += kClusterThreads) rperm[w0 + i] = kv[i];
+  for (int i = threadIdx.x; i < window; i += kClusterThreads) rperm[blockIdx.x * window + i] = kv[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -969,13 +977,12 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
 }
 
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
-                    int window, int leaf, double cx, double cy, cudaStream_t s) {
-  if (rows <= 0 || window > kMaxWindow || window < leaf) return;
-  const int windows = (rows + window - 1) / window;
+                    int window, int n_windows, int leaf, double cx, double cy, cudaStream_t s) {
+  if (rows <= 0 || n_windows <= 0 || window > kMaxWindow || window < leaf) return;
   const int bytes = window * 12;
   cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cluster_kernel<<<windows, kClusterThreads, bytes, s>>>(x, y, rperm, rows_base, rows, window, leaf,
-                                                         cx, cy);
+  cluster_kernel<<<n_windows, kClusterThreads, bytes, s>>>(x, y, rperm, rows_base, rows, window,
+                                                           n_windows, leaf, cx, cy);
 }
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,

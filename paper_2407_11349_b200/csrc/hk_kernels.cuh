@@ -70,12 +70,25 @@ void upload_exp2_table(cudaStream_t s);
 void make_exp2_table(double* out, int n);
 void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
 // Spatially clusters the rows [rows_base, rows_base + rows) window by window
-// (window rows each, k-d median splits down to `leaf` rows) into rperm;
-// positions past the last row hold -1.  Any order gives bitwise the same
-// per-row sums: the clustering only lets the density-scaled trigger skip
-// columns per warp.
+// (k-d median splits down to `leaf` rows) into rperm, `window` (a power of
+// two) slots per window; slots without a row hold -1.  The nblocks row blocks
+// form n_windows windows of near-equal size (window_first_block): a window
+// of few rows would cluster badly.  Any order gives bitwise the same per-row
+// sums: the clustering only lets the density-scaled trigger skip columns per
+// warp.
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
-                    int window, int leaf, double cx, double cy, cudaStream_t s);
+                    int window, int n_windows, int leaf, double cx, double cy, cudaStream_t s);
+// Windows of at most max_blocks row blocks covering nblocks: their number,
+// the first block of window w, and the window of block b.
+__host__ __device__ inline int window_count(int nblocks, int max_blocks) {
+  return (nblocks + max_blocks - 1) / max_blocks;
+}
+__host__ __device__ inline int window_first_block(int w, int nblocks, int n_windows) {
+  return static_cast<int>(static_cast<long long>(w) * nblocks / n_windows);
+}
+__host__ __device__ inline int window_of_block(int b, int nblocks, int n_windows) {
+  return static_cast<int>((static_cast<long long>(b + 1) * n_windows - 1) / nblocks);
+}
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
                  double* partial, int rows_base, int rows_total, bool with_grad, int halves,
                  cudaStream_t s);

@@ -13,6 +13,7 @@ python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err
 python tools/ws_sweep.py 1000000 1 > $O/ws_sweep.log 2>&1
 { python tools/shard_balance.py 1000000 0; python tools/shard_balance.py 1000000 1; } > $O/shard_balance.log 2>&1
 python tools/county_eval.py 1000000 > $O/county.log 2>&1
+python tools/single_precision_eval.py > $O/single.log 2>&1 || true
 if [ "${NCU:-1}" = 1 ]; then
   python bench.py --steps 2 --warmup 1 > $O/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
