@@ -68,11 +68,14 @@ int guarded(Fn&& fn) {
 int row_window(int rows) {
   if (const char* e = std::getenv("HK_ROW_WINDOW")) {
     const int w = std::atoi(e);
-    if (w == 1 || w == 2 || w == 4 || w == 8 || w == 16 || w == 32 || w == 64) return w;
+    if ((w == 1 || w == 2 || w == 4 || w == 8 || w == 16 || w == 32 || w == 64) &&
+        w * hk::rows_per_item(true) <= hk::kMaxClusterWindow)
+      return w;
   }
   const int blocks = (rows + hk::rows_per_item(true) - 1) / hk::rows_per_item(true);
+  const int w_max = std::min(64, hk::kMaxClusterWindow / hk::rows_per_item(true));
   int w = 1;
-  while (w < 64 && 2 * w * 24 <= blocks) w *= 2;
+  while (w < w_max && 2 * w * 24 <= blocks) w *= 2;
   return w;
 }
 

@@ -40,6 +40,8 @@
 
 #include <cassert>
 #include <cstdint>
+#include <stdexcept>
+#include <string>
 
 #include "hk_device.cuh"
 #include "hk_kernels.cuh"
@@ -764,7 +766,7 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
 // row clustering (varying kernel): one CTA per row window
 
 constexpr int kClusterThreads = 1024;
-constexpr int kMaxWindow = 16384;
+// kMaxClusterWindow (hk_kernels.cuh) rows per window at most
 
 // k-d median splits by sorting: the window is sorted by x, each half by y,
 // each quarter by x, ... down to `leaf` rows (one warp's rows).  Every
@@ -786,7 +788,7 @@ __global__ void __launch_bounds__(kClusterThreads)
   const int w0 = window_first_block(blockIdx.x, nblocks, n_windows) * kBI;
   const int w1 = min(rows, window_first_block(blockIdx.x + 1, nblocks, n_windows) * kBI);
   const int window_rows = w1 - w0;
-  HK_ASSERT(window <= kMaxWindow && window % leaf == 0 && window_rows <= window &&
+  HK_ASSERT(window <= kMaxClusterWindow && window % leaf == 0 && window_rows <= window &&
             blockDim.x == kClusterThreads);
   for (int i = threadIdx.x; i < window; i += kClusterThreads) {
     const int li = w0 + i;
@@ -978,7 +980,10 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
 
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, cudaStream_t s) {
-  if (rows <= 0 || n_windows <= 0 || window > kMaxWindow || window < leaf) return;
+  if (rows <= 0 || n_windows <= 0) return;
+  if (window > kMaxClusterWindow || window < leaf || window % leaf)
+    throw std::invalid_argument("launch_cluster: unsupported window of " + std::to_string(window) +
+                                " rows");
   const int bytes = window * 12;
   cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cluster_kernel<<<n_windows, kClusterThreads, bytes, s>>>(x, y, rperm, rows_base, rows, window,

@@ -78,6 +78,7 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
 // warp.
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, cudaStream_t s);
+constexpr int kMaxClusterWindow = 16384;  // rows (192 KB of dynamic shared memory)
 // Windows of at most max_blocks row blocks covering nblocks: their number,
 // the first block of window w, and the window of block b.
 __host__ __device__ inline int window_count(int nblocks, int max_blocks) {
