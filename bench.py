@@ -135,7 +135,7 @@ def run_reference(args):
                                    f"extrapolated x{scale:.0f}; median of {args.steps} samples"},
         "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -199,6 +199,12 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     use_dist = world > 1 or args.force_dist
     if use_dist:
+        if "MASTER_ADDR" not in os.environ:  # --force-dist outside torchrun: loopback rendezvous
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            os.environ["MASTER_ADDR"] = "127.0.0.1"
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     cat = benchmark_catalog(args.n, 42)
@@ -406,12 +412,26 @@ def run_ours(args):
             "clocks": clk,
             "result": {"loglik": ll, "grad": [float(x) for x in g]},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist.is_initialized():
         dist.destroy_process_group()
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    # Libraries (NCCL's version banner, CUDA) may print to fd 1; keep stdout
+    # for the JSON line alone by pointing fd 1 at stderr for the run.
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)

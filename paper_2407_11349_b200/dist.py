@@ -87,7 +87,13 @@ class ShardedLikelihood:
         return reduce_rank_order(partial, self.group)
 
     def eval(self, params: HawkesParams, grad: bool = True):
-        total = self.reduce(self.partial_async(params, grad)).cpu().numpy()
+        total = self.reduce(self.partial_async(params, grad))
+        if self.on_gpu:
+            # the sum lives on the engine's stream: copy it to the host there
+            # (a copy on torch's current stream would not wait for it)
+            with torch.cuda.stream(self.stream):
+                total = total.cpu()
+        total = total.numpy()
         return (float(total[0]), total[1:].copy()) if grad else float(total[0])
 
     # -- cut-posterior location refresh ---------------------------------------

@@ -90,3 +90,17 @@ def test_two_rank_shards_reduce_to_the_whole(oracle, variant):
     want2, gw2 = oracle.ll_grad((cat[0], lon, lat, cat[3]), P, variant)
     assert ll20 == pytest.approx(want2, rel=1e-13)
     np.testing.assert_allclose(g20, gw2, rtol=1e-11, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_nccl_rank_result_is_not_stale():
+    """One NCCL rank (torch.distributed on the GPU): ShardedLikelihood.eval
+    equals Evaluator.eval bitwise across alternating variants, i.e. the host
+    read of the reduced 6-vector is ordered after the engine's stream (a read
+    on torch's current stream returned the previous evaluation)."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    script = Path(__file__).parent / "scripts" / "nccl_single_rank.py"
+    r = subprocess.run([sys.executable, str(script)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
