@@ -4,7 +4,9 @@
 //      fixed-location chain exactly (test_mcmc.cpp:212-231 analogue);
 //   2. posterior agreement: HMC on the GPU and the reference's univariate MH
 //      (CPU) give posterior means within 4 Monte Carlo standard errors on a
-//      simulated catalog (acceptance.cpp:244-296 convention).
+//      simulated catalog (acceptance.cpp:244-296 convention);
+//   3. the HMC chain persists through the reference's chain CSV and sidecar
+//      writers (io.hpp:129-156) and reads back exactly (read_chain_csv).
 // PASS/FAIL lines; exit status = number of failures.
 #include <cmath>
 #include <cstdio>
@@ -12,6 +14,7 @@
 #include <vector>
 
 #include "hawkes/diagnostics.hpp"
+#include "hawkes/io.hpp"
 #include "hawkes/mcmc.hpp"
 #include "hawkes/simulate.hpp"
 #include "hawkes_b200/hmc.hpp"
@@ -87,6 +90,20 @@ void point_regions_collapse() {
   for (std::size_t i = 0; same && i < cut.draws.size(); ++i) same = cut.draws[i] == fixed.draws[i];
   report("point regions: cut-posterior HMC == fixed-location HMC", same,
          std::to_string(cut.draws.size()) + " draws, accepts " + std::to_string(cut.accepts[0]));
+
+  // the reference's chain persistence on the HMC output
+  const std::string csv = "/tmp/hk_test_hmc_chain.csv", side = "/tmp/hk_test_hmc_chain.json";
+  write_chain_csv(csv, cut, cfg.chain.burn_in);
+  write_chain_sidecar(side, cut, 12345);
+  const auto cols = read_chain_csv(csv);
+  bool ok = cols.size() == kParamCount + 1 && cut.loglik_trace.size() == cut.draws.size();
+  for (std::size_t k = 0; ok && k < kParamCount; ++k) {
+    ok = cols[k].size() == cut.draws.size();
+    for (std::size_t i = 0; ok && i < cut.draws.size(); ++i) ok = cols[k][i] == cut.draws[i][k];
+  }
+  for (std::size_t i = 0; ok && i < cut.draws.size(); ++i) ok = cols[kParamCount][i] == cut.loglik_trace[i];
+  report("HMC chain through write_chain_csv / read_chain_csv (io.hpp:129-170)", ok,
+         std::to_string(cut.draws.size()) + " rows");
 }
 
 void posterior_agreement() {
