@@ -769,18 +769,25 @@ constexpr int kClusterThreads = 1024;
 // kMaxClusterWindow (hk_kernels.cuh) rows per window at most
 
 // k-d median splits by sorting: the window is sorted by x, each half by y,
-// each quarter by x, ... down to `leaf` rows (one warp's rows).  Every
-// segment ends ascending, so the padding entries (keys +inf, row -1) end up
-// at the window's tail at every level.
+// each quarter by x, ... down to `leaf` rows (one warp's rows).  Keys are the
+// FP32 coordinates quantised to 16 bits over the locations' bounding box
+// (the splits only need approximate medians) and rows a 16-bit index within
+// the window: 6 bytes per row, so a 32768-row window fits in 192 KB.  Every
+// segment ends ascending, so the padding entries (keys and index 0xffff)
+// end up at the window's tail at every level.
+__device__ __forceinline__ unsigned quantise16(double v, double c, double inv_extent) {
+  const double q = (v - c) * inv_extent * 32767.0 + 32767.5;  // [-extent, extent] -> [0, 65535)
+  return static_cast<unsigned>(fmin(fmax(q, 0.0), 65534.0));
+}
+
 __global__ void __launch_bounds__(kClusterThreads)
     cluster_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm,
                    int rows_base, int rows, int window, int n_windows, int leaf, double cx,
-                   double cy) {
-  // dynamic shared memory (aliases the exp table of other kernels): window
-  // keys x, keys y, rows
-  float* kx = reinterpret_cast<float*>(s_exp2_tab);
-  float* ky = kx + window;
-  int* kv = reinterpret_cast<int*>(ky + window);
+                   double cy, double inv_extent) {
+  // dynamic shared memory (aliases the exp table of other kernels): packed
+  // keys (x << 16 | y) and row indices within the window
+  unsigned* kxy = reinterpret_cast<unsigned*>(s_exp2_tab);
+  unsigned short* kv = reinterpret_cast<unsigned short*>(kxy + window);
   // window blockIdx.x: rows [w0, w1) of the shard, sorted into rperm slots
   // [blockIdx.x * window, + window)
   constexpr int kBI = kThreads * rows_per_thread(true);
@@ -791,31 +798,29 @@ __global__ void __launch_bounds__(kClusterThreads)
   HK_ASSERT(window <= kMaxClusterWindow && window % leaf == 0 && window_rows <= window &&
             blockDim.x == kClusterThreads);
   for (int i = threadIdx.x; i < window; i += kClusterThreads) {
-    const int li = w0 + i;
-    const bool ok = i < window_rows && li < rows;
-    kx[i] = ok ? __double2float_rn(x[rows_base + li] - cx) : __int_as_float(0x7f800000);
-    ky[i] = ok ? __double2float_rn(y[rows_base + li] - cy) : __int_as_float(0x7f800000);
-    kv[i] = ok ? rows_base + li : -1;
+    const bool ok = i < window_rows;
+    const int row = rows_base + w0 + i;
+    kxy[i] = ok ? (quantise16(x[row], cx, inv_extent) << 16) | quantise16(y[row], cy, inv_extent)
+                : 0xffffffffu;
+    kv[i] = ok ? static_cast<unsigned short>(i) : 0xffff;
   }
   __syncthreads();
   int level = 0;
   for (int S = window; S > leaf; S >>= 1, ++level) {
-    const float* key = (level & 1) ? ky : kx;
+    const int shift = (level & 1) ? 0 : 16;  // x first, then y, ...
     for (int k = 2; k <= S; k <<= 1) {
       for (int j = k >> 1; j > 0; j >>= 1) {
         for (int i = threadIdx.x; i < window; i += kClusterThreads) {
           const int l = i ^ j;
           if (l > i) {
             const bool up = k == S || (i & k) == 0;
-            if ((key[i] > key[l]) == up) {
-              const float ax = kx[i], ay = ky[i];
-              const int av = kv[i];
-              kx[i] = kx[l];
-              ky[i] = ky[l];
+            const unsigned a = kxy[i], b = kxy[l];
+            if ((((a >> shift) & 0xffffu) > ((b >> shift) & 0xffffu)) == up) {
+              kxy[i] = b;
+              kxy[l] = a;
+              const unsigned short t = kv[i];
               kv[i] = kv[l];
-              kx[l] = ax;
-              ky[l] = ay;
-              kv[l] = av;
+              kv[l] = t;
             }
           }
         }
@@ -823,7 +828,8 @@ __global__ void __launch_bounds__(kClusterThreads)
       }
     }
   }
-  for (int i = threadIdx.x; i < window; i += kClusterThreads) rperm[blockIdx.x * window + i] = kv[i];
+  for (int i = threadIdx.x; i < window; i += kClusterThreads)
+    rperm[blockIdx.x * window + i] = kv[i] == 0xffff ? -1 : rows_base + w0 + kv[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -979,15 +985,17 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
 }
 
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
-                    int window, int n_windows, int leaf, double cx, double cy, cudaStream_t s) {
+                    int window, int n_windows, int leaf, double cx, double cy, double half_extent,
+                    cudaStream_t s) {
   if (rows <= 0 || n_windows <= 0) return;
   if (window > kMaxClusterWindow || window < leaf || window % leaf)
     throw std::invalid_argument("launch_cluster: unsupported window of " + std::to_string(window) +
                                 " rows");
-  const int bytes = window * 12;
+  const int bytes = window * 6;
+  const double inv_extent = half_extent > 0.0 ? 1.0 / half_extent : 0.0;
   cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cluster_kernel<<<n_windows, kClusterThreads, bytes, s>>>(x, y, rperm, rows_base, rows, window,
-                                                           n_windows, leaf, cx, cy);
+                                                           n_windows, leaf, cx, cy, inv_extent);
 }
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,

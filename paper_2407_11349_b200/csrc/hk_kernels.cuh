@@ -77,8 +77,9 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
 // sums: the clustering only lets the density-scaled trigger skip columns per
 // warp.
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
-                    int window, int n_windows, int leaf, double cx, double cy, cudaStream_t s);
-constexpr int kMaxClusterWindow = 16384;  // rows (192 KB of dynamic shared memory)
+                    int window, int n_windows, int leaf, double cx, double cy, double half_extent,
+                    cudaStream_t s);
+constexpr int kMaxClusterWindow = 32768;  // rows (6 bytes each: 192 KB of dynamic shared memory)
 // Windows of at most max_blocks row blocks covering nblocks: their number,
 // the first block of window w, and the window of block b.
 __host__ __device__ inline int window_count(int nblocks, int max_blocks) {
