@@ -344,11 +344,19 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
   }
 }
 
-__device__ __forceinline__ float ex2_approx(float x) {
+// 2^(x - 24) * 2^24 for the single-precision trigger: MUFU.EX2 in its
+// flush-to-zero form on x + 24 (folded into the caller's argument fma), so no
+// subnormal fix-up instructions; the caller keeps its FP32 tile partial
+// scaled by 2^24 and removes the factor exactly in FP64.  2^(x+24) is normal
+// for every term the unscaled product could keep (x > -150), and below that
+// both round to 0.
+__device__ __forceinline__ float ex2_ftz(float x) {
   float y;
-  asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));  // MUFU.EX2, subnormals kept
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+constexpr float kEx2Shift = 24.0f;
+constexpr double kEx2Unscale = 5.9604644775390625e-08;  // 2^-24
 
 // Precision::single trigger of a BT/BTx/T tile (the reference's float path,
 // model.hpp:183-208 / :271-296, evaluated with MUFU ex2): FP32 distances in
@@ -376,7 +384,7 @@ __device__ __forceinline__ void tile_trig_f32(RowState<NR>& R, const double* __r
           const float dx = R.xf[r] - fj.x, dy = R.yf[r] - fj.y;
           const float d2 = fmaf(dx, dx, dy * dy);
           if (!__any_sync(0xffffffffu, d2 <= fj.z)) continue;
-          Tp[r] = fmaf(kw.y, ex2_approx(d2 * kw.x), Tp[r]);
+          Tp[r] = fmaf(kw.y, ex2_ftz(fmaf(d2, kw.x, kEx2Shift)), Tp[r]);
         }
       }
     }
@@ -388,7 +396,7 @@ __device__ __forceinline__ void tile_trig_f32(RowState<NR>& R, const double* __r
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         const float dx = R.xf[r] - fj.x, dy = R.yf[r] - fj.y;
-        Tp[r] = fmaf(kw.y, ex2_approx(fmaf(dx, dx, dy * dy) * kw.x), Tp[r]);
+        Tp[r] = fmaf(kw.y, ex2_ftz(fmaf(fmaf(dx, dx, dy * dy), kw.x, kEx2Shift)), Tp[r]);
       }
     }
   }
@@ -396,7 +404,7 @@ __device__ __forceinline__ void tile_trig_f32(RowState<NR>& R, const double* __r
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const double E = exp2_16<kMode>(R.t[r] - t_ref, c.Kw);
-    R.T[r] = fma(E, static_cast<double>(Tp[r]), R.T[r]);
+    R.T[r] = fma(E, static_cast<double>(Tp[r]) * kEx2Unscale, R.T[r]);  // the 2^24 of ex2_ftz
   }
 }
 
