@@ -50,7 +50,7 @@ namespace hk {
 #define HK_ROWS_VAR 2
 #endif
 #ifndef HK_UNROLL
-#define HK_UNROLL 2
+#define HK_UNROLL 4
 #endif
 constexpr int kThreads = HK_THREADS;  // threads per CTA
 __host__ __device__ constexpr int rows_per_thread(bool varying) {
