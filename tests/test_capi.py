@@ -77,6 +77,30 @@ def test_create_validates_before_touching_the_device():
     assert rc == 1 and b"times not sorted at index 1" in lib.hk_last_error()
 
 
+def test_variant_entry_points_validate():
+    """hk_plan_shards_variant / hk_create_variant: an unknown variant is an
+    invalid_argument (before any device work); both variants plan valid,
+    different shard boundaries."""
+    from paper_2407_11349_b200._lib import lib
+    from paper_2407_11349_b200 import benchmark_catalog
+    t = benchmark_catalog(50000, 3).t
+    b = np.zeros(5, dtype=np.uintp)
+    assert lib.hk_plan_shards_variant(t, len(t), 4, 7, b) == 1
+    assert b"unknown variant" in lib.hk_last_error()
+    b0, b1 = np.zeros(5, dtype=np.uintp), np.zeros(5, dtype=np.uintp)
+    assert lib.hk_plan_shards_variant(t, len(t), 4, 0, b0) == 0
+    assert lib.hk_plan_shards_variant(t, len(t), 4, 1, b1) == 0
+    for bb in (b0, b1):
+        assert bb[0] == 0 and bb[-1] == len(t) and np.all(np.diff(bb.astype(np.int64)) > 0)
+    assert not np.array_equal(b0, b1)
+    b2 = np.zeros(5, dtype=np.uintp)
+    assert lib.hk_plan_shards(t, len(t), 4, b2) == 0 and np.array_equal(b2, b0)
+    z = np.zeros(2)
+    h = C.c_void_p()
+    assert lib.hk_create_variant(np.array([0.0, 1.0]), z, z, np.ones(2), 2, 1, 5, C.byref(h)) == 1
+    assert b"unknown variant" in lib.hk_last_error()
+
+
 def test_make_builds_sm100a():
     """The shared library carries sm_100a SASS (cross-compiled here)."""
     from paper_2407_11349_b200 import _lib
