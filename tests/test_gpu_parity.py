@@ -237,6 +237,28 @@ def test_adversarial_finite(eng, oracle):
     assert ll == pytest.approx(oracle.ll_grad(same.arrays(), [1.0] * 6, 0)[0], rel=1e-12)
 
 
+@pytest.mark.parametrize("window", ["8", "2"])
+def test_adversarial_density_scaled_clustered(eng, oracle, monkeypatch, window):
+    """The adversarial catalogs on the density-scaled kernel with the row
+    clustering on: every location identical (zero extent: all cluster keys
+    tie), locations 1e4 degrees apart (the quantised keys span a huge box),
+    and all times tied; each against the oracle."""
+    monkeypatch.setenv("HK_ROW_WINDOW", window)
+    n = 12000
+    rng = np.random.default_rng(5)
+    d = np.exp(rng.uniform(0, 6, n))
+    p = dict(mu0=1.0, tau_t=1.0, xi0=1.0, sigma_x=1e-3, sigma_t=1.0, area=1.0)
+    coincident = eng.Catalog(np.arange(n) * 0.01, np.full(n, 0.5), np.full(n, 0.5), d)
+    run_vs_oracle(eng, oracle, coincident.arrays(), p, 1)
+    i = np.arange(n)
+    sep = eng.Catalog(i * 0.01, np.where(i % 2, 1.0, -1.0) * 1e4 + rng.normal(0, 1e-3, n),
+                      np.where(i % 3, 1.0, -1.0) * 1e4 + rng.normal(0, 1e-3, n), d)
+    run_vs_oracle(eng, oracle, sep.arrays(), dict(p, sigma_x=0.5), 1)
+    tied = eng.Catalog(np.zeros(n), rng.uniform(-1, 1, n), rng.uniform(-1, 1, n), d)
+    ll = eng.Evaluator(tied).eval(hp(eng, p, 1))
+    assert ll == pytest.approx(oracle.ll_grad(tied.arrays(), p, 1)[0], rel=1e-12)
+
+
 def test_random_params_sweep(eng, oracle):
     """Random catalogs and parameters over the reference test ranges,
     including sizes around the 256-row/column tile edges."""
