@@ -530,10 +530,15 @@ __device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
   }
 }
 
-template <bool kVarying, bool kGrad, int kMode, bool kF32>
-__global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)))
+// kBgOnly: the background-only launches of the homogeneous plan (workspace
+// tau refreshes, the density-scaled evaluation's background) as their own
+// instantiation, with the trigger compiled out (fewer registers: 4 CTAs/SM).
+// Same source, same arithmetic: bitwise the background of a full launch.
+template <bool kVarying, bool kGrad, int kMode, bool kF32, bool kBgOnly = false>
+__global__ void __launch_bounds__(kThreads, kBgOnly ? 4 : min_blocks(rows_per_thread(kVarying)))
     pair_kernel(const PairParams P) {
   constexpr int NR = rows_per_thread(kVarying);
+#define HK_HALVES (kBgOnly ? kHalfBg : P.halves)  // (kept inline: same code as before when !kBgOnly)
   __shared__ __align__(128) double s_buf[2][kSlots * kBJ];
   constexpr bool kUseF = kVarying || kF32;  // FP32 column data staged
   __shared__ __align__(128) float4 s_fbuf[kUseF ? 2 : 1][kUseF ? kBJ : 1];
@@ -630,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
   HK_ASSERT(ntl >= 0 && ntl <= kMaxItemTiles && it.te * kBJ <= P.d.npad);
   for (int k = tid; k < ntl; k += kThreads) {
     const int ta = tile_type_all(it.tb + k, bi, P);
-    s_cls[k] = static_cast<unsigned char>(restrict_type(ta, P.halves) | (ta << 4));
+    s_cls[k] = static_cast<unsigned char>(restrict_type(ta, HK_HALVES) | (ta << 4));
   }
   __syncthreads();
   // Unit sequence (warp-uniform state): runs of expansion tiles (full class
@@ -682,7 +687,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     const double* buf = s_buf[stage];
     const float4* fbuf = s_fbuf[kUseF ? stage : 0];
     const float2* kwbuf = s_kwbuf[kF32 ? stage : 0];
-    if (kF32 && (cur.type == kTileBT || cur.type == kTileT)) {
+    if constexpr (kBgOnly) {  // classes restricted to B, Bx and M
+      if (cur.type == kTileB)
+        tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, fbuf, P.c);
+      else if (cur.type == kTileBx)
+        bg_expansion<NR, kGrad, kMode>(R, buf, cur.cnt * kBJ, bi, P.c, s_red);
+      else
+        tile_masked<NR, kVarying, kGrad, kMode, true, false>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
+    } else if (kF32 && (cur.type == kTileBT || cur.type == kTileT)) {
       if (cur.type == kTileBT) tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, fbuf, P.c);
       tile_trig_f32<NR, kVarying, kMode>(R, buf + sT * kBJ, fbuf, kwbuf, P.c);
     } else switch (cur.type) {
@@ -722,16 +734,17 @@ __global__ void __launch_bounds__(kThreads, min_blocks(rows_per_thread(kVarying)
     HK_ASSERT(row >= P.rows_base && row < P.rows_base + P.rows_total);
     HK_ASSERT(row >= it.rb && row < it.re);  // the item's own block / window
     const size_t i = static_cast<size_t>(row - P.rows_base);
-    if (P.halves & kHalfBg) {  // only this launch's half (split plans share the buffer)
+    if (HK_HALVES & kHalfBg) {  // only this launch's half (split plans share the buffer)
       out[0 * plane + i] = R.B[r];
       out[1 * plane + i] = R.B2[r];
     }
-    if (P.halves & kHalfTr) {
+    if (!kBgOnly && (P.halves & kHalfTr)) {
       out[2 * plane + i] = R.T[r];
       out[3 * plane + i] = R.Td[r];
       out[4 * plane + i] = R.Tq[r];
     }
   }
+#undef HK_HALVES
 }
 
 // ---------------------------------------------------------------------------
@@ -969,13 +982,13 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* sink, int iters
   if (r == 12345.678) sink[threadIdx.x] = r;
 }
 
-template <bool V, bool G, int M, bool F>
+template <bool V, bool G, int M, bool F, bool B = false>
 void launch_pair_t(const PairParams& P, int n_items, cudaStream_t s) {
   constexpr int kTabBytes = kTab * static_cast<int>(sizeof(double));  // dynamic: the exp table
   // static + dynamic exceed the default 48 KB: opt in (on the current device)
-  cudaFuncSetAttribute(pair_kernel<V, G, M, F>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(pair_kernel<V, G, M, F, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        kTabBytes);
-  pair_kernel<V, G, M, F><<<n_items, kThreads, kTabBytes, s>>>(P);
+  pair_kernel<V, G, M, F, B><<<n_items, kThreads, kTabBytes, s>>>(P);
 }
 
 }  // namespace
@@ -1011,6 +1024,17 @@ void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, i
                  cudaStream_t s) {
   if (n_items <= 0) return;
   PairParams P{d, c, items, partial, rows_base, rows_total, halves};
+  if (halves == kHalfBg && !c.varying) {  // background only, homogeneous plan (FP64 either way)
+    switch ((with_grad && !c.single_prec ? 3 : 0) + c.mode) {
+      case 0: launch_pair_t<false, false, kExact, false, true>(P, n_items, s); break;
+      case 1: launch_pair_t<false, false, kFlush, false, true>(P, n_items, s); break;
+      case 2: launch_pair_t<false, false, kChecked, false, true>(P, n_items, s); break;
+      case 3: launch_pair_t<false, true, kExact, false, true>(P, n_items, s); break;
+      case 4: launch_pair_t<false, true, kFlush, false, true>(P, n_items, s); break;
+      default: launch_pair_t<false, true, kChecked, false, true>(P, n_items, s); break;
+    }
+    return;
+  }
   if (c.single_prec) {  // Precision::single: LL only
     const int key = (c.varying ? 3 : 0) + c.mode;
     switch (key) {
