@@ -530,15 +530,19 @@ __device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
   }
 }
 
-// kBgOnly: the background-only launches of the homogeneous plan (workspace
-// tau refreshes, the density-scaled evaluation's background) as their own
-// instantiation, with the trigger compiled out (fewer registers: 4 CTAs/SM).
-// Same source, same arithmetic: bitwise the background of a full launch.
-template <bool kVarying, bool kGrad, int kMode, bool kF32, bool kBgOnly = false>
-__global__ void __launch_bounds__(kThreads, kBgOnly ? 4 : min_blocks(rows_per_thread(kVarying)))
+// kOnly: single-half launches as their own instantiations, the other half
+// compiled out (fewer registers, more resident CTAs).  1 = background only
+// (homogeneous plan: workspace tau refreshes and the density-scaled
+// evaluation's background), 2 = trigger only (the density-scaled trigger
+// launch).  Same source, same arithmetic: bitwise the halves of a full launch.
+template <bool kVarying, bool kGrad, int kMode, bool kF32, int kOnly = 0>
+__global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
+                                            : kOnly == 2 ? HK_MIN_BLOCKS_TRIG
+                                                         : min_blocks(rows_per_thread(kVarying)))
     pair_kernel(const PairParams P) {
   constexpr int NR = rows_per_thread(kVarying);
-#define HK_HALVES (kBgOnly ? kHalfBg : P.halves)  // (kept inline: same code as before when !kBgOnly)
+  constexpr bool kBgOnly = kOnly == 1, kTrOnly = kOnly == 2;
+#define HK_HALVES (kBgOnly ? kHalfBg : kTrOnly ? kHalfTr : P.halves)  // inline: unchanged code for kOnly 0
   __shared__ __align__(128) double s_buf[2][kSlots * kBJ];
   constexpr bool kUseF = kVarying || kF32;  // FP32 column data staged
   __shared__ __align__(128) float4 s_fbuf[kUseF ? 2 : 1][kUseF ? kBJ : 1];
@@ -694,6 +698,15 @@ __global__ void __launch_bounds__(kThreads, kBgOnly ? 4 : min_blocks(rows_per_th
         bg_expansion<NR, kGrad, kMode>(R, buf, cur.cnt * kBJ, bi, P.c, s_red);
       else
         tile_masked<NR, kVarying, kGrad, kMode, true, false>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
+    } else if constexpr (kTrOnly) {  // classes restricted to T and M
+      if (cur.type == kTileT) {
+        if (kF32)
+          tile_trig_f32<NR, kVarying, kMode>(R, buf + sT * kBJ, fbuf, kwbuf, P.c);
+        else
+          tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, fbuf, P.c);
+      } else {
+        tile_masked<NR, kVarying, kGrad, kMode, false, true>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
+      }
     } else if (kF32 && (cur.type == kTileBT || cur.type == kTileT)) {
       if (cur.type == kTileBT) tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, fbuf, P.c);
       tile_trig_f32<NR, kVarying, kMode>(R, buf + sT * kBJ, fbuf, kwbuf, P.c);
@@ -738,7 +751,7 @@ __global__ void __launch_bounds__(kThreads, kBgOnly ? 4 : min_blocks(rows_per_th
       out[0 * plane + i] = R.B[r];
       out[1 * plane + i] = R.B2[r];
     }
-    if (!kBgOnly && (P.halves & kHalfTr)) {
+    if (!kBgOnly && (HK_HALVES & kHalfTr)) {
       out[2 * plane + i] = R.T[r];
       out[3 * plane + i] = R.Td[r];
       out[4 * plane + i] = R.Tq[r];
@@ -982,7 +995,7 @@ __global__ void __launch_bounds__(256) dfma_probe_kernel(double* sink, int iters
   if (r == 12345.678) sink[threadIdx.x] = r;
 }
 
-template <bool V, bool G, int M, bool F, bool B = false>
+template <bool V, bool G, int M, bool F, int B = 0>
 void launch_pair_t(const PairParams& P, int n_items, cudaStream_t s) {
   constexpr int kTabBytes = kTab * static_cast<int>(sizeof(double));  // dynamic: the exp table
   // static + dynamic exceed the default 48 KB: opt in (on the current device)
@@ -1026,12 +1039,27 @@ void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, i
   PairParams P{d, c, items, partial, rows_base, rows_total, halves};
   if (halves == kHalfBg && !c.varying) {  // background only, homogeneous plan (FP64 either way)
     switch ((with_grad && !c.single_prec ? 3 : 0) + c.mode) {
-      case 0: launch_pair_t<false, false, kExact, false, true>(P, n_items, s); break;
-      case 1: launch_pair_t<false, false, kFlush, false, true>(P, n_items, s); break;
-      case 2: launch_pair_t<false, false, kChecked, false, true>(P, n_items, s); break;
-      case 3: launch_pair_t<false, true, kExact, false, true>(P, n_items, s); break;
-      case 4: launch_pair_t<false, true, kFlush, false, true>(P, n_items, s); break;
-      default: launch_pair_t<false, true, kChecked, false, true>(P, n_items, s); break;
+      case 0: launch_pair_t<false, false, kExact, false, 1>(P, n_items, s); break;
+      case 1: launch_pair_t<false, false, kFlush, false, 1>(P, n_items, s); break;
+      case 2: launch_pair_t<false, false, kChecked, false, 1>(P, n_items, s); break;
+      case 3: launch_pair_t<false, true, kExact, false, 1>(P, n_items, s); break;
+      case 4: launch_pair_t<false, true, kFlush, false, 1>(P, n_items, s); break;
+      default: launch_pair_t<false, true, kChecked, false, 1>(P, n_items, s); break;
+    }
+    return;
+  }
+  if (halves == kHalfTr && c.varying) {  // density-scaled trigger only
+    const int key = c.single_prec ? 6 + c.mode : (with_grad ? 3 : 0) + c.mode;
+    switch (key) {
+      case 0: launch_pair_t<true, false, kExact, false, 2>(P, n_items, s); break;
+      case 1: launch_pair_t<true, false, kFlush, false, 2>(P, n_items, s); break;
+      case 2: launch_pair_t<true, false, kChecked, false, 2>(P, n_items, s); break;
+      case 3: launch_pair_t<true, true, kExact, false, 2>(P, n_items, s); break;
+      case 4: launch_pair_t<true, true, kFlush, false, 2>(P, n_items, s); break;
+      case 5: launch_pair_t<true, true, kChecked, false, 2>(P, n_items, s); break;
+      case 6: launch_pair_t<true, false, kExact, true, 2>(P, n_items, s); break;
+      case 7: launch_pair_t<true, false, kFlush, true, 2>(P, n_items, s); break;
+      default: launch_pair_t<true, false, kChecked, true, 2>(P, n_items, s); break;
     }
     return;
   }
