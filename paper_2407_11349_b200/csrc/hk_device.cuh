@@ -62,7 +62,7 @@ __host__ __device__ constexpr int rows_per_item(bool varying) {
 }
 // resident CTAs per SM the register budget is sized for (64K regs)
 #ifndef HK_MIN_BLOCKS_TRIG
-#define HK_MIN_BLOCKS_TRIG 5  // density-scaled trigger-only launches
+#define HK_MIN_BLOCKS_TRIG 6  // density-scaled trigger-only launches
 #endif
 #ifndef HK_MIN_BLOCKS_CONST
 #define HK_MIN_BLOCKS_CONST 3

@@ -83,6 +83,19 @@ constexpr double kDBetaMax = 4.0;  // |2 D beta| bound: column factors stay belo
 // Shared-memory slots of one staged tile.
 enum Slot { sT = 0, sX, sY, sW, sV, sZ, sK, sAux, kSlots };
 
+// Stage-buffer position of each logical slot.  The compact layout (kC) is
+// the trigger-only launches': T tiles stage x, y, w, v, z, K (their reference
+// time is read from global memory) and M tiles t, x, y, K, q in the w/v
+// positions, 6 slots instead of 8, so 6 CTAs fit per SM.
+template <bool kC>
+__host__ __device__ constexpr int slot_pos(int s) {
+  if (!kC) return s;
+  constexpr int m[kSlots] = {2, 0, 1, 2, 3, 4, 5, 3};  // T X Y W V Z K Aux
+  return m[s];
+}
+template <bool kC>
+constexpr int kStageSlots = kC ? 6 : kSlots;
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -184,7 +197,7 @@ __device__ __forceinline__ int tile_type_all(int J, const BlockInfo& bi, const P
   return kTileM;
 }
 
-template <bool kVarying, bool kGrad, bool kF32>
+template <bool kVarying, bool kGrad, bool kF32, bool kC = false>
 __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf, float4* fbuf,
                                            float2* kwbuf, uint64_t* bar, const PairParams& P) {
   const int j0 = J * kBJ;
@@ -200,8 +213,8 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
   if (kF32 && (type == kTileBT || type == kTileBTx || type == kTileT)) {
     // single precision: times (FP64 background / row factors) + the FP32
     // trigger columns {x, y, thr} and {K, w}
-    mbar_expect_tx(bar, kBytes + kBJ * (sizeof(float4) + sizeof(float2)));
-    bulk_g2s(buf + sT * kBJ, P.d.t + j0, kBytes, bar);
+    mbar_expect_tx(bar, (kC ? 0u : kBytes) + kBJ * (sizeof(float4) + sizeof(float2)));
+    if (!kC) bulk_g2s(buf + sT * kBJ, P.d.t + j0, kBytes, bar);
     bulk_g2s(fbuf, P.d.fxy + j0, kBJ * sizeof(float4), bar);
     bulk_g2s(kwbuf, P.d.fkw + j0, kBJ * sizeof(float2), bar);
     return;
@@ -211,8 +224,8 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
   } else if (type == kTileM) {
     mask = (1u << sT) | (1u << sX) | (1u << sY);
     if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = q
-  } else {  // BT, BTx or T
-    mask = (1u << sT) | (1u << sX) | (1u << sY) | (1u << sW);
+  } else {  // BT, BTx or T (compact: t_ref from global memory, no times)
+    mask = (kC ? 0u : (1u << sT)) | (1u << sX) | (1u << sY) | (1u << sW);
     if (kGrad) mask |= (1u << sV);
     if (kVarying) mask |= 1u << sK;
     if (kVarying && kGrad) mask |= (1u << sZ);
@@ -224,7 +237,7 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
                                type == kTileM ? P.d.q : P.d.thr};
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
-    if (mask & (1u << s)) bulk_g2s(buf + s * kBJ, src[s] + j0, kBytes, bar);
+    if (mask & (1u << s)) bulk_g2s(buf + slot_pos<kC>(s) * kBJ, src[s] + j0, kBytes, bar);
 }
 
 template <int R>
@@ -254,16 +267,17 @@ __device__ __forceinline__ unsigned warp_candidates(const RowState<NR>& R,
 }
 
 // BT / B / T tiles: no per-pair guards.
-template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr>
+template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr, bool kC = false>
 __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restrict__ buf,
-                                          const float4* __restrict__ fbuf, const EvalCoef& c) {
-  const double* __restrict__ st = buf + sT * kBJ;
-  const double* __restrict__ sx = buf + sX * kBJ;
-  const double* __restrict__ sy = buf + sY * kBJ;
-  const double* __restrict__ sw = buf + sW * kBJ;
-  const double* __restrict__ sv = buf + sV * kBJ;
-  const double* __restrict__ sz = buf + sZ * kBJ;
-  const double* __restrict__ sk = buf + sK * kBJ;
+                                          const float4* __restrict__ fbuf, const EvalCoef& c,
+                                          double t_ref_c = 0.0 /* kC: the tile's last time */) {
+  const double* __restrict__ st = buf + slot_pos<kC>(sT) * kBJ;
+  const double* __restrict__ sx = buf + slot_pos<kC>(sX) * kBJ;
+  const double* __restrict__ sy = buf + slot_pos<kC>(sY) * kBJ;
+  const double* __restrict__ sw = buf + slot_pos<kC>(sW) * kBJ;
+  const double* __restrict__ sv = buf + slot_pos<kC>(sV) * kBJ;
+  const double* __restrict__ sz = buf + slot_pos<kC>(sZ) * kBJ;
+  const double* __restrict__ sk = buf + slot_pos<kC>(sK) * kBJ;
   const double Kb = c.Kb, Kq0 = c.Kq0;
   double Tp[NR], Vp[NR], Qp[NR];
 #pragma unroll
@@ -330,7 +344,7 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
     }
   }
   if (kTr) {
-    const double t_ref = st[kBJ - 1];
+    const double t_ref = kC ? t_ref_c : st[kBJ - 1];
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const double dt = R.t[r] - t_ref;  // >= 0 on BT/T tiles
@@ -362,10 +376,11 @@ constexpr double kEx2Unscale = 5.9604644775390625e-08;  // 2^-24
 // model.hpp:183-208 / :271-296, evaluated with MUFU ex2): FP32 distances in
 // the centred frame, FP32 partial sums within the tile, then the FP64 row
 // factor exp(-omega (t_i - t_ref)) and an FP64 accumulator across tiles.
-template <int NR, bool kVarying, int kMode>
+template <int NR, bool kVarying, int kMode, bool kC = false>
 __device__ __forceinline__ void tile_trig_f32(RowState<NR>& R, const double* __restrict__ st,
                                               const float4* __restrict__ fbuf,
-                                              const float2* __restrict__ kwbuf, const EvalCoef& c) {
+                                              const float2* __restrict__ kwbuf, const EvalCoef& c,
+                                              double t_ref_c = 0.0) {
   float Tp[NR];
 #pragma unroll
   for (int r = 0; r < NR; ++r) Tp[r] = 0.f;
@@ -400,7 +415,7 @@ __device__ __forceinline__ void tile_trig_f32(RowState<NR>& R, const double* __r
       }
     }
   }
-  const double t_ref = st[kBJ - 1];
+  const double t_ref = kC ? t_ref_c : st[kBJ - 1];
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const double E = exp2_16<kMode>(R.t[r] - t_ref, c.Kw);
@@ -480,15 +495,15 @@ __device__ __forceinline__ void bg_expansion(RowState<NR>& R, const double* __re
 // this launch needs.  Density-scaled trigger: only the warp's candidate
 // columns (warp_candidates; a dropped column's spatial exponent alone is
 // beyond the flush threshold, so its term is an exact 0 for every row).
-template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr>
+template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr, bool kC = false>
 __device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
                                             const double* __restrict__ buf,
                                             const float4* __restrict__ fbuf, const EvalCoef& c) {
-  const double* __restrict__ st = buf + sT * kBJ;
-  const double* __restrict__ sx = buf + sX * kBJ;
-  const double* __restrict__ sy = buf + sY * kBJ;
-  const double* __restrict__ sk = buf + sK * kBJ;
-  const double* __restrict__ sq = buf + sAux * kBJ;
+  const double* __restrict__ st = buf + slot_pos<kC>(sT) * kBJ;
+  const double* __restrict__ sx = buf + slot_pos<kC>(sX) * kBJ;
+  const double* __restrict__ sy = buf + slot_pos<kC>(sY) * kBJ;
+  const double* __restrict__ sk = buf + slot_pos<kC>(sK) * kBJ;
+  const double* __restrict__ sq = buf + slot_pos<kC>(sAux) * kBJ;
   const double Kb = c.Kb, Kq0 = c.Kq0, Kw = c.Kw;
   for (int cc = 0; cc < kBJ; cc += 32) {
     const unsigned cand = (kTr && kVarying) ? warp_candidates(R, fbuf, cc) : 0xffffffffu;
@@ -543,12 +558,13 @@ __global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
   constexpr int NR = rows_per_thread(kVarying);
   constexpr bool kBgOnly = kOnly == 1, kTrOnly = kOnly == 2;
 #define HK_HALVES (kBgOnly ? kHalfBg : kTrOnly ? kHalfTr : P.halves)  // inline: unchanged code for kOnly 0
-  __shared__ __align__(128) double s_buf[2][kSlots * kBJ];
+  constexpr bool kC = kOnly == 2;  // compact stage layout (trigger-only launches)
+  __shared__ __align__(128) double s_buf[2][kStageSlots<kC> * kBJ];
   constexpr bool kUseF = kVarying || kF32;  // FP32 column data staged
   __shared__ __align__(128) float4 s_fbuf[kUseF ? 2 : 1][kUseF ? kBJ : 1];
   __shared__ __align__(128) float2 s_kwbuf[kF32 ? 2 : 1][kF32 ? kBJ : 1];
   __shared__ __align__(8) uint64_t s_bar[2];
-  __shared__ double s_red[kThreads / 32][kNM];
+  __shared__ double s_red[kC ? 1 : kThreads / 32][kNM];  // background reduction (unused if kC)
   __shared__ unsigned char s_cls[kMaxItemTiles];
 
   const int tid = threadIdx.x;
@@ -678,12 +694,12 @@ __global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
   int stage = 0;
   unsigned phases = 0u;  // bit s = parity of the next wait on stage s
   if (cur.cnt && tid == 0)
-    issue_tile<kVarying, kGrad, kF32>(cur.type, cur.J, cur.cnt, s_buf[0], s_fbuf[0], s_kwbuf[0],
+    issue_tile<kVarying, kGrad, kF32, kC>(cur.type, cur.J, cur.cnt, s_buf[0], s_fbuf[0], s_kwbuf[0],
                                       &s_bar[0], P);
   while (cur.cnt) {
     const Unit nxt = unit_next();
     if (nxt.cnt && tid == 0)
-      issue_tile<kVarying, kGrad, kF32>(nxt.type, nxt.J, nxt.cnt, s_buf[stage ^ 1],
+      issue_tile<kVarying, kGrad, kF32, kC>(nxt.type, nxt.J, nxt.cnt, s_buf[stage ^ 1],
                                         s_fbuf[kUseF ? stage ^ 1 : 0], s_kwbuf[kF32 ? stage ^ 1 : 0],
                                         &s_bar[stage ^ 1], P);
     mbar_wait(&s_bar[stage], (phases >> stage) & 1u);
@@ -698,14 +714,16 @@ __global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
         bg_expansion<NR, kGrad, kMode>(R, buf, cur.cnt * kBJ, bi, P.c, s_red);
       else
         tile_masked<NR, kVarying, kGrad, kMode, true, false>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
-    } else if constexpr (kTrOnly) {  // classes restricted to T and M
+    } else if constexpr (kTrOnly) {  // classes restricted to T and M; compact stage layout
       if (cur.type == kTileT) {
+        const double t_ref = P.d.t[cur.J * kBJ + kBJ - 1];  // the tile's last time
         if (kF32)
-          tile_trig_f32<NR, kVarying, kMode>(R, buf + sT * kBJ, fbuf, kwbuf, P.c);
+          tile_trig_f32<NR, kVarying, kMode, kC>(R, nullptr, fbuf, kwbuf, P.c, t_ref);
         else
-          tile_fast<NR, kVarying, kGrad, kMode, false, true>(R, buf, fbuf, P.c);
+          tile_fast<NR, kVarying, kGrad, kMode, false, true, kC>(R, buf, fbuf, P.c, t_ref);
       } else {
-        tile_masked<NR, kVarying, kGrad, kMode, false, true>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
+        tile_masked<NR, kVarying, kGrad, kMode, false, true, kC>(R, cur.J * kBJ, P.d.n, buf, fbuf,
+                                                                  P.c);
       }
     } else if (kF32 && (cur.type == kTileBT || cur.type == kTileT)) {
       if (cur.type == kTileBT) tile_fast<NR, kVarying, kGrad, kMode, true, false>(R, buf, fbuf, P.c);
