@@ -95,6 +95,7 @@ struct DeviceState {
   double *K = nullptr, *thr = nullptr, *w = nullptr, *v = nullptr, *z = nullptr;
   float4* fxy = nullptr;
   float2* fkw = nullptr;
+  double2 *xy = nullptr, *wk = nullptr, *vz = nullptr;  // interleaved trigger columns
   int *lb = nullptr, *ub = nullptr;
   // clustered row order of the varying plan (hk::launch_cluster), valid for
   // location version rperm_loc
@@ -117,7 +118,7 @@ struct DeviceState {
   std::size_t prof_used = 0;
 
   hk::DeviceCatalog catalog(int n, int npad) const {
-    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z, fxy, fkw, rperm};
+    return hk::DeviceCatalog{n, npad, t, x, y, q, lb, ub, K, thr, w, v, z, fxy, fkw, rperm, xy, wk, vz};
   }
 };
 
@@ -164,6 +165,8 @@ struct hk_ctx {
         if (p) cudaFree(p);
       if (s.fxy) cudaFree(s.fxy);
       if (s.fkw) cudaFree(s.fkw);
+      for (double2* p2 : {s.xy, s.wk, s.vz})
+        if (p2) cudaFree(p2);
       if (s.lb) cudaFree(s.lb);
       if (s.ub) cudaFree(s.ub);
       if (s.rperm) cudaFree(s.rperm);
@@ -228,6 +231,9 @@ struct hk_ctx {
     s.z = dmalloc<double>(npad);
     s.fxy = dmalloc<float4>(npad);
     s.fkw = dmalloc<float2>(npad);
+    s.xy = dmalloc<double2>(npad);
+    s.wk = dmalloc<double2>(npad);
+    s.vz = dmalloc<double2>(npad);
     s.lb = dmalloc<int>(n);
     s.ub = dmalloc<int>(n);
     upload_padded(s, s.t, t, t[n - 1]);

@@ -83,16 +83,16 @@ constexpr double kDBetaMax = 4.0;  // |2 D beta| bound: column factors stay belo
 // Shared-memory slots of one staged tile.
 enum Slot { sT = 0, sX, sY, sW, sV, sZ, sK, sAux, kSlots };
 
-// Stage-buffer position of each logical slot.  The compact layout (kC) is
-// the trigger-only launches': T tiles stage x, y, w, v, z, K (their reference
-// time is read from global memory) and M tiles t, x, y, K, q in the w/v
-// positions, 6 slots instead of 8, so 6 CTAs fit per SM.
+// Stage-buffer position of each logical slot (the full layout).  The
+// compact layout (kC) is the trigger-only launches': 6 slots instead of 8, so
+// 6 CTAs fit per SM, holding interleaved pairs so that a pair's column data
+// is three 16-byte broadcast loads.  T tiles: {x,y} {w,K} {v,z} (their
+// reference time is read from global memory); M tiles: {x,y} {w,K} t q.
 template <bool kC>
 __host__ __device__ constexpr int slot_pos(int s) {
-  if (!kC) return s;
-  constexpr int m[kSlots] = {2, 0, 1, 2, 3, 4, 5, 3};  // T X Y W V Z K Aux
-  return m[s];
+  return s;
 }
+enum CompactSlot { cXY = 0, cWK = 2, cVZ = 4, cT = 4, cQ = 5 };
 template <bool kC>
 constexpr int kStageSlots = kC ? 6 : kSlots;
 
@@ -210,6 +210,25 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
     return;
   }
   unsigned mask = 0;
+  if constexpr (kC) {
+    if (!(kF32 && type == kTileT)) {
+      constexpr unsigned kPair = 2 * kBytes;
+      const bool m = type == kTileM;
+      const unsigned bytes = 2 * kPair + (m ? (kVarying ? 2 : 1) * kBytes : (kGrad ? kPair : 0u)) +
+                             (kVarying ? kBJ * sizeof(float4) : 0u);
+      mbar_expect_tx(bar, bytes);
+      if (kVarying) bulk_g2s(fbuf, P.d.fxy + j0, kBJ * sizeof(float4), bar);
+      bulk_g2s(buf + cXY * kBJ, P.d.xy + j0, kPair, bar);
+      bulk_g2s(buf + cWK * kBJ, P.d.wk + j0, kPair, bar);
+      if (m) {
+        bulk_g2s(buf + cT * kBJ, P.d.t + j0, kBytes, bar);
+        if (kVarying) bulk_g2s(buf + cQ * kBJ, P.d.q + j0, kBytes, bar);
+      } else if (kGrad) {
+        bulk_g2s(buf + cVZ * kBJ, P.d.vz + j0, kPair, bar);
+      }
+      return;
+    }
+  }
   if (kF32 && (type == kTileBT || type == kTileBTx || type == kTileT)) {
     // single precision: times (FP64 background / row factors) + the FP32
     // trigger columns {x, y, thr} and {K, w}
@@ -224,8 +243,8 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
   } else if (type == kTileM) {
     mask = (1u << sT) | (1u << sX) | (1u << sY);
     if (kVarying) mask |= (1u << sK) | (1u << sAux);  // aux = q
-  } else {  // BT, BTx or T (compact: t_ref from global memory, no times)
-    mask = (kC ? 0u : (1u << sT)) | (1u << sX) | (1u << sY) | (1u << sW);
+  } else {  // BT, BTx or T
+    mask = (1u << sT) | (1u << sX) | (1u << sY) | (1u << sW);
     if (kGrad) mask |= (1u << sV);
     if (kVarying) mask |= 1u << sK;
     if (kVarying && kGrad) mask |= (1u << sZ);
@@ -327,8 +346,17 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
       while (cand) {  // warp-uniform
         const int j = c + __ffs(cand) - 1;
         cand &= cand - 1u;
-        const double xj = sx[j], yj = sy[j], kj = sk[j], wj = sw[j];
-        const double vj = kGrad ? sv[j] : 0.0, zj = kGrad ? sz[j] : 0.0;
+        double xj, yj, kj, wj, vj, zj;
+        if constexpr (kC) {  // interleaved pairs: three 16-byte broadcast loads
+          const double2 xy = reinterpret_cast<const double2*>(buf + cXY * kBJ)[j];
+          const double2 wk = reinterpret_cast<const double2*>(buf + cWK * kBJ)[j];
+          const double2 vz = kGrad ? reinterpret_cast<const double2*>(buf + cVZ * kBJ)[j]
+                                   : make_double2(0.0, 0.0);
+          xj = xy.x, yj = xy.y, wj = wk.x, kj = wk.y, vj = vz.x, zj = vz.y;
+        } else {
+          xj = sx[j], yj = sy[j], kj = sk[j], wj = sw[j];
+          vj = kGrad ? sv[j] : 0.0, zj = kGrad ? sz[j] : 0.0;
+        }
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
           const double dx = R.x[r] - xj, dy = R.y[r] - yj;
@@ -499,11 +527,13 @@ template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr, bool
 __device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
                                             const double* __restrict__ buf,
                                             const float4* __restrict__ fbuf, const EvalCoef& c) {
-  const double* __restrict__ st = buf + slot_pos<kC>(sT) * kBJ;
-  const double* __restrict__ sx = buf + slot_pos<kC>(sX) * kBJ;
-  const double* __restrict__ sy = buf + slot_pos<kC>(sY) * kBJ;
-  const double* __restrict__ sk = buf + slot_pos<kC>(sK) * kBJ;
-  const double* __restrict__ sq = buf + slot_pos<kC>(sAux) * kBJ;
+  const double* __restrict__ st = buf + (kC ? cT : sT) * kBJ;
+  const double* __restrict__ sx = buf + sX * kBJ;
+  const double* __restrict__ sy = buf + sY * kBJ;
+  const double* __restrict__ sk = buf + sK * kBJ;
+  const double* __restrict__ sq = buf + (kC ? cQ : sAux) * kBJ;
+  const double2* __restrict__ cxy = reinterpret_cast<const double2*>(buf + cXY * kBJ);
+  const double2* __restrict__ cwk = reinterpret_cast<const double2*>(buf + cWK * kBJ);
   const double Kb = c.Kb, Kq0 = c.Kq0, Kw = c.Kw;
   for (int cc = 0; cc < kBJ; cc += 32) {
     const unsigned cand = (kTr && kVarying) ? warp_candidates(R, fbuf, cc) : 0xffffffffu;
@@ -527,9 +557,9 @@ __device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
         }
         if (tr_col) {
           const double qj = kVarying ? sq[j] : 1.0;
-          const double Kj = kVarying ? sk[j] : Kq0;
+          const double Kj = kVarying ? (kC ? cwk[j].y : sk[j]) : Kq0;
           const bool tr_ok = jg < R.lb[r];  // t_j < t_i
-          const double dx = R.x[r] - sx[j], dy = R.y[r] - sy[j];
+          const double dx = R.x[r] - (kC ? cxy[j].x : sx[j]), dy = R.y[r] - (kC ? cxy[j].y : sy[j]);
           const double d2 = fma(dx, dx, dy * dy);
           const double A = fma(d2, Kj, td * Kw);
           const double e = exp2_16_arg<kMode>(A);
@@ -803,9 +833,15 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
                            0.f);
     d.fkw[j] = make_float2(__double2float_rn(-(c.half_s2 * q) * 1.4426950408889634),
                            __double2float_rn(w));
+    d.xy[j] = make_double2(d.x[j], d.y[j]);
+    d.wk[j] = make_double2(w, K);
+    d.vz[j] = make_double2(dtr * w, q * w);
   } else {
     d.fxy[j] = make_float4(0.f, 0.f, -1.f, 0.f);
     d.fkw[j] = make_float2(0.f, 0.f);
+    d.xy[j] = make_double2(0.0, 0.0);
+    d.wk[j] = make_double2(0.0, -1.0);
+    d.vz[j] = make_double2(0.0, 0.0);
     d.K[j] = -1.0;
     d.thr[j] = 0.0;
     d.w[j] = 0.0;

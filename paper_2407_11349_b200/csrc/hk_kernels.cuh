@@ -58,6 +58,9 @@ struct DeviceCatalog {
   float4* fxy;       // prep: {x_j - cx, y_j - cy, thrf_j, 0} in FP32     [npad]
   float2* fkw;       // prep: {K_j log2(e)/(ln2-units), w_j} in FP32 (single precision) [npad]
   const int* rperm;  // clustered row order per row window (Item::pos), or null
+  double2* xy;       // prep: {x_j, y_j}  \ interleaved copies for the trigger-only
+  double2* wk;       // prep: {w_j, K_j}   > launches' compact stage layout: one
+  double2* vz;       // prep: {v_j, z_j}  / 16-byte broadcast load per pair    [npad]
 };
 
 // Row-sum halves: the background [B, B2] and the trigger [T, Td, Tq].
