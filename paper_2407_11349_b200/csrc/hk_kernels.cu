@@ -83,15 +83,11 @@ constexpr double kDBetaMax = 4.0;  // |2 D beta| bound: column factors stay belo
 // Shared-memory slots of one staged tile.
 enum Slot { sT = 0, sX, sY, sW, sV, sZ, sK, sAux, kSlots };
 
-// Stage-buffer position of each logical slot (the full layout).  The
-// compact layout (kC) is the trigger-only launches': 6 slots instead of 8, so
-// 6 CTAs fit per SM, holding interleaved pairs so that a pair's column data
-// is three 16-byte broadcast loads.  T tiles: {x,y} {w,K} {v,z} (their
-// reference time is read from global memory); M tiles: {x,y} {w,K} t q.
-template <bool kC>
-__host__ __device__ constexpr int slot_pos(int s) {
-  return s;
-}
+// The compact stage layout (kC) of the trigger-only launches: 6 slots
+// instead of 8, so 6 CTAs fit per SM, holding interleaved pairs so that a
+// pair's column data is three 16-byte broadcast loads.  T tiles: {x,y} {w,K}
+// {v,z} (their reference time is read from global memory); M tiles: {x,y}
+// {w,K} t q.  Slot positions (in units of kBJ doubles):
 enum CompactSlot { cXY = 0, cWK = 2, cVZ = 4, cT = 4, cQ = 5 };
 template <bool kC>
 constexpr int kStageSlots = kC ? 6 : kSlots;
@@ -256,7 +252,7 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
                                type == kTileM ? P.d.q : P.d.thr};
 #pragma unroll
   for (int s = 0; s < kSlots; ++s)
-    if (mask & (1u << s)) bulk_g2s(buf + slot_pos<kC>(s) * kBJ, src[s] + j0, kBytes, bar);
+    if (mask & (1u << s)) bulk_g2s(buf + s * kBJ, src[s] + j0, kBytes, bar);
 }
 
 template <int R>
@@ -290,13 +286,13 @@ template <int NR, bool kVarying, bool kGrad, int kMode, bool kBg, bool kTr, bool
 __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restrict__ buf,
                                           const float4* __restrict__ fbuf, const EvalCoef& c,
                                           double t_ref_c = 0.0 /* kC: the tile's last time */) {
-  const double* __restrict__ st = buf + slot_pos<kC>(sT) * kBJ;
-  const double* __restrict__ sx = buf + slot_pos<kC>(sX) * kBJ;
-  const double* __restrict__ sy = buf + slot_pos<kC>(sY) * kBJ;
-  const double* __restrict__ sw = buf + slot_pos<kC>(sW) * kBJ;
-  const double* __restrict__ sv = buf + slot_pos<kC>(sV) * kBJ;
-  const double* __restrict__ sz = buf + slot_pos<kC>(sZ) * kBJ;
-  const double* __restrict__ sk = buf + slot_pos<kC>(sK) * kBJ;
+  const double* __restrict__ st = buf + sT * kBJ;
+  const double* __restrict__ sx = buf + sX * kBJ;
+  const double* __restrict__ sy = buf + sY * kBJ;
+  const double* __restrict__ sw = buf + sW * kBJ;
+  const double* __restrict__ sv = buf + sV * kBJ;
+  const double* __restrict__ sz = buf + sZ * kBJ;
+  const double* __restrict__ sk = buf + sK * kBJ;
   const double Kb = c.Kb, Kq0 = c.Kq0;
   double Tp[NR], Vp[NR], Qp[NR];
 #pragma unroll
