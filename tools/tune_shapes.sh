@@ -7,7 +7,7 @@ CSRC=paper_2407_11349_b200/csrc
 for spec in "$@"; do
   IFS=: read name th rows un mb tb <<< "$spec"
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xptxas -v \
-    -DHK_THREADS=$th -DHK_ROWS_CONST=$rows -DHK_ROWS_VAR=$mb -DHK_UNROLL=$un -DHK_TAB_BITS=${tb:-4} \
+    -DHK_THREADS=$th -DHK_ROWS_CONST=$rows -DHK_ROWS_VAR=$mb -DHK_UNROLL=$un -DHK_TAB_BITS=${tb:-8} \
     -shared $CSRC/hk_kernels.cu $CSRC/hk_capi.cu $CSRC/hk_host.cpp -o build/tune/lib_$name.so \
     2> build/tune/ptxas_$name.log &
 done
