@@ -109,11 +109,17 @@ def sample_rows(n, k):
 
 
 def run_reference(args):
+    """The reference's own CPU path (oracle/_ref: the unmodified reference
+    headers) on the host cores.  Only oracle/ libraries load in this process:
+    the catalog comes from the reference's benchmark_catalog too."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_2407_11349_b200 import benchmark_catalog
-    cat = benchmark_catalog(args.n, 42).arrays()
+    from oracle.oracle import Reference, ref_available
+    if ref_available():
+        cat = Reference().benchmark_catalog(args.n, 42)
+    else:  # the C restatement's generator is not built; numpy mirror of the same draws is not bitwise
+        raise SystemExit("bench.py --impl reference needs oracle/_ref (make -C oracle ref)")
     rows = sample_rows(args.n, args.cpu_rows)
     v = 1 if args.variant == "varying" else 0
     cpu_sample_time(cat, v, rows[: max(1, len(rows) // 8)], steps=max(1, args.warmup))  # warm-up
@@ -183,6 +189,54 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+COUNTS = ROOT / "profiles" / "r02_fp64_counts.json"
+
+
+def lib_sha():
+    import hashlib
+    return hashlib.sha256((ROOT / "paper_2407_11349_b200" / "libhawkes_b200.so").read_bytes()).hexdigest()[:16]
+
+
+def measured_counts(tag):
+    """FP64-pipe instructions and DRAM bytes of one pair launch from the
+    committed ncu capture of the same workload (tools/capture_counts.py:
+    sm__inst_executed_pipe_fp64.sum x 32 thread slots, dram__bytes_*.sum);
+    the counts are a property of (build, catalog, params), deterministic."""
+    if not COUNTS.exists():
+        return None
+    d = json.loads(COUNTS.read_text())
+    c = d.get("launches", {}).get(tag)
+    if c is None:
+        return None
+    return dict(c, stale=d.get("lib_sha16") != lib_sha(), source=str(COUNTS.relative_to(ROOT)))
+
+
+def roofline(tag, launch_ms, fp64_peak, pairs, algorithmic_bytes):
+    """Roofline of the dominant pair launch: achieved = FP64-pipe thread
+    instructions executed per launch (ncu count, FMA-equivalent, 2 flop each)
+    / the launch's live CUDA-event duration; peak = this GPU's measured DFMA
+    throughput; frac = achieved / peak = FP64-pipe utilisation."""
+    c = measured_counts(tag)
+    r = {"bound": "fp64", "kernel": tag, "unit": "TFLOP/s", "peak": fp64_peak,
+         "peak_source": "measured in this run: register-resident DFMA loop (hk_measure_fp64_peak, "
+                        "2 flop per DFMA); MEASURED_PEAKS.json has no FP64 figure",
+         "launch_ms": launch_ms, "algorithmic_bytes": algorithmic_bytes}
+    if c is None:
+        r.update(achieved=None, frac=None, traffic=None, note="no committed ncu count for this workload")
+        return r
+    slots = c["fp64_warp_inst"] * 32.0
+    achieved = 2.0 * slots / (launch_ms * 1e-3) / 1e12
+    r.update(achieved=achieved, frac=achieved / fp64_peak, traffic=c["dram_bytes"],
+             fp64_thread_inst_per_launch=slots, fp64_inst_per_pair=slots / pairs,
+             algorithmic_speedup=FP64_PER_PAIR / (slots / pairs),
+             counts={"source": c["source"], "stale": c["stale"], "ncu_duration_ms": c["duration_ms"],
+                     "ncu_fp64_pipe_pct": c.get("fp64_pipe_pct")},
+             convention=f"achieved counts the FP64-pipe instructions the kernel actually executes "
+                        f"(ncu); algorithmic_speedup = {FP64_PER_PAIR} FP64 per ordered pair (SURVEY.md 8d, "
+                        "direct evaluation with a libm-style exp) / executed per pair")
+    return r
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -208,9 +262,8 @@ def run_ours(args):
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
     cat = benchmark_catalog(args.n, 42)
-    p = HawkesParams(**BENCH_PARAMS, variant=Variant[args.variant])
     if use_dist:
-        sh = ShardedLikelihood(cat, device=local, variant=p.variant)
+        sh = ShardedLikelihood(cat, device=local, variant=Variant[args.variant])
         ev, stream = sh.ev, sh.stream
     else:
         sh = None
@@ -225,7 +278,7 @@ def run_ours(args):
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
-    def step(params=p):
+    def step(params):
         with torch.cuda.stream(stream):
             flush.zero_()
         if sh is not None:
@@ -233,144 +286,121 @@ def run_ours(args):
         else:
             ev.eval_async(params, True)
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    ev.reset_profile()
-    ev.set_profiling(True)
-    if use_dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local) if rank == 0 else None
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        e0.record()
-    for _ in range(args.steps):
-        step()
-    with torch.cuda.stream(stream):
-        e1.record()
-    torch.cuda.synchronize()
-    if use_dist:
-        dist.barrier()
-    clk = clocks.stop() if clocks else None
-    ms_total = e0.elapsed_time(e1)
-    pair_ms, pair_launches, launches = ev.profile()
-    ev.set_profiling(False)
-    t = torch.tensor([ms_total, pair_ms / max(pair_launches, 1)], dtype=torch.float64, device=dev)
-    if use_dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total, pair_ms_avg = float(t[0]), float(t[1])
+    def maxr(*vals):
+        t = torch.tensor(vals, dtype=torch.float64, device=dev)
+        if use_dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return [float(v) for v in t]
 
-    # ---- the same step on the direct per-pair path (background expansion
-    # off): the pure O(N^2) kernel, for the FP64-pipe roofline of SURVEY 8(d)
-    direct_steps = 2
-    ev.set_bg_expansion(False)
-    step()
-    torch.cuda.synchronize()
-    ev.reset_profile()
-    ev.set_profiling(True)
-    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        d0.record()
-    for _ in range(direct_steps):
-        step()
-    with torch.cuda.stream(stream):
-        d1.record()
-    torch.cuda.synchronize()
-    dpair_ms, dpair_n, _ = ev.profile()
-    ev.set_profiling(False)
-    ev.set_bg_expansion(True)
-    t = torch.tensor([d0.elapsed_time(d1), dpair_ms / max(dpair_n, 1)], dtype=torch.float64, device=dev)
-    if use_dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    direct_ms_total, direct_pair_ms = float(t[0]), float(t[1])
-    # ---- the other kernel variant on the same catalog (config 4, the
-    # density-scaled lengthscale, when the headline is homogeneous)
-    other = "varying" if args.variant == "constant" else "constant"
-    p_other = HawkesParams(**BENCH_PARAMS, variant=Variant[other])
-    other_steps = 3
-    for _ in range(2):
-        step(p_other)
-    torch.cuda.synchronize()
-    ev.reset_profile()
-    ev.set_profiling(True)
-    o0, o1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with torch.cuda.stream(stream):
-        o0.record()
-    for _ in range(other_steps):
-        step(p_other)
-    with torch.cuda.stream(stream):
-        o1.record()
-    torch.cuda.synchronize()
-    opair_ms, opair_n, _ = ev.profile()
-    ev.set_profiling(False)
-    t = torch.tensor([o0.elapsed_time(o1), opair_ms / max(opair_n, 1)], dtype=torch.float64, device=dev)
-    if use_dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    other_ms_total, other_pair_ms = float(t[0]), float(t[1])
+    def timed(params, steps, warmup, sample_clocks=False):
+        """Device time of `steps` evaluations (CUDA events on the engine's
+        stream, barrier + synchronize both sides, max over ranks) and the
+        pair launches' time by kind."""
+        for _ in range(warmup):
+            step(params)
+        torch.cuda.synchronize()
+        ev.reset_profile()
+        ev.set_profiling(True)
+        if use_dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks = ClockSampler(local) if (rank == 0 and sample_clocks) else None
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record()
+        for _ in range(steps):
+            step(params)
+        with torch.cuda.stream(stream):
+            e1.record()
+        torch.cuda.synchronize()
+        if use_dist:
+            dist.barrier()
+        clk = clocks.stop() if clocks else None
+        kms, kn = ev.profile_kinds()
+        _, _, launches = ev.profile()
+        ev.set_profiling(False)
+        per_kind = [kms[k] / max(kn[k], 1) for k in range(3)]
+        ms_total, *per_kind = maxr(e0.elapsed_time(e1), *per_kind)
+        return ms_total, per_kind, int(launches), clk
 
-    # result of the last step, for the record
-    if sh is not None:
-        ll, g = sh.eval(p, grad=True)
-    else:
-        ll, g = ev.eval(p, grad=True)
-
-    # ---- e2e through the public API: pinned-host locations in, result out
     pin = torch.empty(2, args.n, dtype=torch.float64).pin_memory()
     pin.numpy()[0] = cat.lon
     pin.numpy()[1] = cat.lat
     lon_h, lat_h = pin.numpy()[0], pin.numpy()[1]
 
-    def e2e_step():
-        if sh is not None:
-            sh.set_locations(lon_h, lat_h) if rank == 0 else sh.set_locations()
-            return sh.eval(p, grad=True)
-        ev.set_locations(lon_h, lat_h)
-        return ev.eval(p, grad=True)
+    def e2e(params, steps):
+        """Through the public API: each step copies the (re-sampled)
+        locations from pinned host memory, evaluates LL + gradient and reads
+        the result back to the host."""
+        def one():
+            if sh is not None:
+                sh.set_locations(lon_h, lat_h) if rank == 0 else sh.set_locations()
+                return sh.eval(params, grad=True)
+            ev.set_locations(lon_h, lat_h)
+            return ev.eval(params, grad=True)
+        one()
+        if use_dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            res = one()
+        return maxr(time.perf_counter() - t0)[0], res
 
-    e2e_step()
-    if use_dist:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        e2e_step()
-    e2e_s = time.perf_counter() - t0
-    t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if use_dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_s = float(t[0])
+    n = args.n
+    pairs = n * (n - 1)
+    rows_local = ev.rows()
+    pairs_local = (rows_local[1] - rows_local[0]) * (n - 1)
+    p_main = HawkesParams(**BENCH_PARAMS, variant=Variant[args.variant])
+    other = "varying" if args.variant == "constant" else "constant"
+    p_other = HawkesParams(**BENCH_PARAMS, variant=Variant[other])
+
+    ms_total, kinds, launches, clk = timed(p_main, args.steps, args.warmup, sample_clocks=True)
+    e2e_s, (ll, g) = e2e(p_main, args.steps)
+    o_ms, o_kinds, o_launches, _ = timed(p_other, args.steps, args.warmup)
+    o_e2e_s, (o_ll, o_g) = e2e(p_other, args.steps)
+
+    # the direct per-pair path (background expansion off): the pure O(N^2)
+    # kernel, one evaluation
+    ev.set_bg_expansion(False)
+    d_ms, d_kinds, _, _ = timed(HawkesParams(**BENCH_PARAMS, variant=Variant.constant), 1, 1)
+    ev.set_bg_expansion(True)
 
     if rank == 0:
-        n = args.n
-        pairs = n * (n - 1)
-        value = args.steps / (ms_total * 1e-3)
-        rows_local = ev.rows()
-        pairs_local = (rows_local[1] - rows_local[0]) * (n - 1)
-        achieved = pairs_local * FP64_PER_PAIR * 2 / (pair_ms_avg * 1e-3) / 1e12
-        # the pair kernel's DRAM traffic per launch from the committed ncu capture
-        traffic, ncu = None, {}
-        prof = ROOT / "profiles" / "r01_pair_kernel_ncu.json"
-        if prof.exists():
-            d = json.loads(prof.read_text())
-            tag = f"{args.variant}_{n}"
-            traffic = d.get("dram_bytes_per_launch", {}).get(tag)
-            for cap in d.get("captures", []):
-                if cap.get("tag") == tag and cap.get("duration_ms"):
-                    pipe = cap["fp64_pipe_pct"] / 100.0
-                    fp64_per_pair = (pipe * 2 * 148 * cap["sm_clock_ghz"] * 1e9 * cap["duration_ms"] * 1e-3
-                                     * 32 / pairs_local)
-                    ncu = {"fp64_pipe_active": pipe, "fp64_instr_per_pair_executed": fp64_per_pair,
-                           "source": "profiles/r01_pair_kernel_ncu.json (ncu --set full, same build)"}
-        cpu = None
-        if world == 1:
+        def cpu(variant_id):
+            if world != 1:
+                return None
             rows = sample_rows(n, args.cpu_rows)
-            times, kind, threads = cpu_sample_time(cat.arrays(), int(p.variant), rows, steps=1)
-            cpu_eval_s = times[0] * n / len(rows)
-            cpu = {"value": 1.0 / cpu_eval_s, "unit": "evals/s", "cores": threads, "kind": kind,
-                   "cpu": cpu_model(),
-                   "sample": f"{len(rows)} evenly spaced rows of N={n} through the reference's "
-                             f"slice_log_likelihood (LL only: no gradient in the reference), "
-                             f"extrapolated x{n / len(rows):.0f}"}
+            times, kind, threads = cpu_sample_time(cat.arrays(), variant_id, rows, steps=1)
+            return {"value": 1.0 / (times[0] * n / len(rows)), "unit": "evals/s", "cores": threads,
+                    "kind": kind, "cpu": cpu_model(),
+                    "sample": f"{len(rows)} evenly spaced rows of N={n} through the reference's "
+                              f"slice_log_likelihood (LL only: no gradient in the reference), "
+                              f"extrapolated x{n / len(rows):.0f}"}
+
+        # algorithmic bytes of a pair launch: the catalog columns it reads
+        # (t, x, y, w, v; + K, z for the density-scaled trigger) once and the
+        # five row sums it writes once
+        def algo_bytes(variant, kind):
+            cols = {"both": 5, "bg": 1, "trigger": 7 if variant == "varying" else 5}[kind]
+            outs = {"both": 5, "bg": 2, "trigger": 3}[kind]
+            return (cols + outs) * 8 * (rows_local[1] - rows_local[0])
+
+        def pair_line(variant, kinds_ms):
+            if variant == "constant":
+                return roofline(f"constant_{n}_both", kinds_ms[0], fp64_peak, pairs_local,
+                                algo_bytes(variant, "both"))
+            return roofline(f"varying_{n}_trigger", kinds_ms[2], fp64_peak, pairs_local,
+                            algo_bytes(variant, "trigger"))
+
+        def launches_ms(variant, kinds_ms):
+            return ({"pair_both_ms": kinds_ms[0]} if variant == "constant" else
+                    {"pair_background_ms": kinds_ms[1], "pair_trigger_ms": kinds_ms[2]})
+
+        value = args.steps / (ms_total * 1e-3)
+        o_value = args.steps / (o_ms * 1e-3)
+        e2e_note = ("per step: hk_set_locations from pinned host (lon, lat) + LL+grad + result read to host"
+                    + ("; locations broadcast over NCCL" if world > 1 else ""))
         line = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_total / args.steps,
@@ -378,39 +408,32 @@ def run_ours(args):
             "data": "synthetic", "config": workload(args, world),
             "pairs_per_sec": value * pairs,
             "e2e": {"value": args.steps / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": 2 * n * 8,
-                    "d2h_bytes_per_step": 6 * 8,
-                    "note": "per step: hk_set_locations from pinned host (lon, lat) + LL+grad + "
-                            "result read to host" + ("; locations broadcast over NCCL" if world > 1 else "")},
-            "gpu_launches": int(launches),
-            "roofline": {"bound": "fp64", "kernel": "pair_kernel", "achieved": achieved,
-                         "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                         "traffic": traffic,
-                         "peak_source": "measured in this run: register-resident DFMA loop "
-                                        "(hk_measure_fp64_peak); MEASURED_PEAKS.json has no FP64 figure",
-                         "convention": f"{FP64_PER_PAIR} FP64-pipe instructions per ordered pair "
-                                       "(SURVEY.md 8d: direct evaluation, libm-style exp), 2 flop each; "
-                                       f"pair kernel avg {pair_ms_avg:.2f} ms over {pairs_local:.3e} pairs/launch. "
-                                       "frac > 1 because the kernel needs fewer FP64 instructions per pair "
-                                       "than the convention (exact background block expansion + 64-entry-table "
-                                       "exp); the pipe's real utilisation is `ncu.fp64_pipe_active`",
-                         "ncu": ncu},
-            "direct_kernel": {
-                "note": "the same LL+grad step with the background block expansion disabled "
-                        "(HK_OPT_BG_EXPANSION=0): every ordered pair evaluated directly",
-                "value": direct_steps / (direct_ms_total * 1e-3), "unit": "evals/s",
-                "ms_per_step": direct_ms_total / direct_steps,
-                "roofline": {"bound": "fp64", "achieved": pairs_local * FP64_PER_PAIR * 2 / (direct_pair_ms * 1e-3) / 1e12,
-                             "peak": fp64_peak, "unit": "TFLOP/s",
-                             "frac": pairs_local * FP64_PER_PAIR * 2 / (direct_pair_ms * 1e-3) / 1e12 / fp64_peak}},
-            ("density_scaled" if other == "varying" else "homogeneous"): {
-                "note": f"the same LL+grad step with the {other} kernel on the same catalog "
-                        f"(BASELINE config {4 if other == 'varying' else 3}), device-timed like `value`",
-                "variant": other, "value": other_steps / (other_ms_total * 1e-3), "unit": "evals/s",
-                "ms_per_step": other_ms_total / other_steps, "pair_kernel_ms": other_pair_ms,
-                "pairs_per_sec": other_steps / (other_ms_total * 1e-3) * pairs},
-            "cpu_baseline": cpu,
+                    "d2h_bytes_per_step": 6 * 8, "note": e2e_note},
+            "gpu_launches": launches,
+            "launches_ms": launches_ms(args.variant, kinds),
+            "roofline": pair_line(args.variant, kinds),
+            "cpu_baseline": cpu(int(p_main.variant)),
             "clocks": clk,
             "result": {"loglik": ll, "grad": [float(x) for x in g]},
+            ("density_scaled" if other == "varying" else "homogeneous"): {
+                "note": f"BASELINE config {4 if other == 'varying' else 3}: the same LL+grad step with the "
+                        f"{other} kernel on the same catalog, measured like the headline (device-timed "
+                        f"`value`, `e2e` through the public API, roofline of its dominant pair launch)",
+                "variant": other, "value": o_value, "unit": "evals/s", "ms_per_step": o_ms / args.steps,
+                "pairs_per_sec": o_value * pairs,
+                "e2e": {"value": args.steps / o_e2e_s, "unit": "evals/s", "h2d_bytes_per_step": 2 * n * 8,
+                        "d2h_bytes_per_step": 6 * 8, "note": e2e_note},
+                "gpu_launches": o_launches,
+                "launches_ms": launches_ms(other, o_kinds),
+                "roofline": pair_line(other, o_kinds),
+                "cpu_baseline": cpu(int(p_other.variant)),
+                "result": {"loglik": o_ll, "grad": [float(x) for x in o_g]}},
+            "direct_kernel": {
+                "note": "one homogeneous LL+grad evaluation with the background block expansion disabled "
+                        "(HK_OPT_BG_EXPANSION=0): every ordered pair evaluated directly",
+                "ms_per_step": d_ms, "pair_both_ms": d_kinds[0],
+                "roofline": roofline(f"direct_{n}_both", d_kinds[0], fp64_peak, pairs_local,
+                                     algo_bytes("constant", "both"))},
         }
         emit(line)
     if dist.is_initialized():

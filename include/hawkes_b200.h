@@ -9,7 +9,7 @@
  *     Partition, Precision)     engine.hpp:101-110   (grad5 == NULL: LL only)
  *   log_likelihood_t / slice_log_likelihood        hk_eval_rows
  *                               engine.hpp:65-99
- *   event_contribution          model.hpp:351-356  hk_eval_rows(b, b+1)
+ *   event_contribution          model.hpp:225-230  hk_eval_rows(b, b+1)
  *   LikelihoodWorkspace<double>::set_locations     hk_set_locations
  *                               engine.hpp:172-178
  *   LikelihoodWorkspace<double>::evaluate_*        hk_ws_eval (device-cached
@@ -84,6 +84,17 @@ int hk_create(const double* t, const double* lon, const double* lat, const doubl
 int hk_create_variant(const double* t, const double* lon, const double* lat, const double* density,
                       size_t n, int n_gpus, int variant, hk_ctx** out);
 
+/* hk_create_variant over an explicit device list: shard k (cost-balanced)
+ * runs on devices[k].  Over distinct devices the per-evaluation 6-vectors
+ * are all-gathered with NCCL (libnccl.so.2, loaded on first use) and summed
+ * on the devices in device order, and hk_set_locations copies to devices[0]
+ * once and NCCL-broadcasts to the rest.  A list that repeats a device (e.g.
+ * {0, 0, 0, 0}: several shards on one GPU) moves the same data with CUDA
+ * peer copies instead (also forced by HK_NO_NCCL=1); results are bitwise
+ * identical between the two and deterministic. */
+int hk_create_devices(const double* t, const double* lon, const double* lat, const double* density,
+                      size_t n, const int* devices, int n_devices, int variant, hk_ctx** out);
+
 /* One rank's shard for a one-process-per-GPU job: the full catalog is
  * uploaded to `device`, but only rows [row_begin, row_end) are evaluated.
  * hk_eval then returns this shard's partial sums; the caller reduces the
@@ -94,17 +105,30 @@ int hk_create_shard(const double* t, const double* lon, const double* lat, const
 void hk_destroy(hk_ctx* ctx);
 
 /* Replaces the event locations (LikelihoodWorkspace::set_locations,
- * engine.hpp:172-178): host arrays of length n, copied to every device. */
+ * engine.hpp:172-178): host arrays of length n (pinned memory makes the copy
+ * asynchronous DMA), copied to the first device, checked there (a device
+ * reduction: bounding box and finiteness; a non-finite location fails with
+ * the reference's Catalog message and leaves the context without valid
+ * locations) and broadcast to the other devices (NCCL). */
 int hk_set_locations(hk_ctx* ctx, const double* lon, const double* lat);
 
-/* Same, from device arrays already resident on the context's device (e.g.
- * after an NCCL broadcast); single-device contexts only. */
+/* Same, from device arrays resident on the context's first device (e.g. a
+ * GPU location sampler's output, hk_resample_locations). */
 int hk_set_locations_device(hk_ctx* ctx, const double* lon_device, const double* lat_device);
 
 /* Full evaluation.  *ll receives the log-likelihood (sum over the context's
- * rows of ell_n, engine.hpp:65-99 / model.hpp:340-349).  If grad5 != NULL it
+ * rows of ell_n, engine.hpp:65-99 / model.hpp:214-223).  If grad5 != NULL it
  * receives d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t).  Synchronous. */
 int hk_eval(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5);
+
+/* hk_eval that also returns the per-row terms of the SAME launches (the
+ * production plan: clustered windows, split background/trigger launches):
+ * ell_rows[k] = ell_n and, if grad_rows != NULL (requires grad5),
+ * grad_rows[5k..5k+4] = d ell_n / d theta for the context's rows in order
+ * (hk_rows: begin + k).  Either row pointer may be NULL.  For parity checks
+ * of the full-evaluation path row by row. */
+int hk_eval_detail(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5, double* ell_rows,
+                   double* grad_rows);
 
 /* Precision::single (engine.hpp:106-109 with EvalData<float>): the
  * trigger pair sums in FP32 (centred FP32 coordinates, MUFU ex2, FP32
@@ -123,12 +147,18 @@ int hk_eval_single(hk_ctx* ctx, const hk_params* p, double* ll);
  * hk_set_locations only the trigger.  force != 0 recomputes both halves
  * (evaluate_full).  Results are bitwise identical to hk_eval's. */
 int hk_ws_eval(hk_ctx* ctx, const hk_params* p, int force, double* ll, double* grad5);
-/* Cache hits / misses of hk_ws_eval since creation. */
+/* LikelihoodWorkspace<float> (engine.hpp:117-229 with Real = float): the
+ * hk_eval_single arithmetic with the same two-entry caches per half (keyed
+ * separately from the double entries).  LL only.  Bitwise equal to
+ * hk_eval_single at the same parameters. */
+int hk_ws_eval_single(hk_ctx* ctx, const hk_params* p, int force, double* ll);
+/* Cache hits / misses of hk_ws_eval / hk_ws_eval_single since creation. */
 int hk_ws_stats(const hk_ctx* ctx, long* hits, long* misses);
 
-/* Asynchronous form: enqueues the evaluation on the context's stream and
+/* Asynchronous form: enqueues the evaluation on the context's stream(s) and
  * leaves [ll, g_mu0, g_tau_t, g_xi0, g_sigma_x, g_sigma_t] in a device buffer
- * (hk_result_device).  Single-device contexts only. */
+ * on the first device (hk_result_device; multi-device contexts: the
+ * device-order sum after the all-gather). */
 int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad);
 /* Device pointer to the 6-double result of the last hk_eval_async. */
 const double* hk_result_device(hk_ctx* ctx);
@@ -159,6 +189,11 @@ int hk_rows(const hk_ctx* ctx, size_t* begin, size_t* end, int* n_devices);
 int hk_set_profiling(hk_ctx* ctx, int enable);
 int hk_profile(hk_ctx* ctx, double* pair_kernel_ms, long* pair_launches, long* total_launches);
 int hk_reset_profile(hk_ctx* ctx);
+/* The same events split by launch kind: [0] pair launches computing both
+ * halves, [1] background-only launches, [2] trigger-only launches (the
+ * density-scaled plan runs one [1] and one [2] per evaluation).  ms3 and
+ * launches3 have 3 entries each. */
+int hk_profile_kinds(hk_ctx* ctx, double* ms3, long* launches3);
 
 /* Catalog invariants (types.hpp:43-57) and HawkesParams::validate
  * (types.hpp:92-103) on their own, with the reference's messages. */

@@ -6,7 +6,7 @@
 // mirrors the reference signatures, semantics and exception types:
 //
 //   hawkes::log_likelihood                   engine.hpp:101-110
-//   hawkes::event_contribution               model.hpp:351-356
+//   hawkes::event_contribution               model.hpp:225-230
 //   hawkes::LikelihoodWorkspace<double>      engine.hpp:117-229
 //   (new) log_likelihood_and_gradient
 //
@@ -23,7 +23,10 @@
 
 #include <array>
 #include <cstddef>
+#include <cstdint>
+#include <cstring>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
@@ -121,6 +124,14 @@ class Engine {
     return ll;
   }
 
+  // The same caches over the single-precision arithmetic (hk_ws_eval_single).
+  double workspace_eval_single(const HawkesParams& p, Variant v, bool force) {
+    const hk_params c = detail::to_c(p, v);
+    double ll = 0.0;
+    detail::check(hk_ws_eval_single(ctx_.get(), &c, force ? 1 : 0, &ll));
+    return ll;
+  }
+
  private:
   std::unique_ptr<hk_ctx, void (*)(hk_ctx*)> ctx_;
 };
@@ -131,27 +142,76 @@ inline void check_call(const Catalog& catalog, const HawkesParams& p, const Part
     throw std::invalid_argument("log_likelihood: partition does not cover the catalog");
 }
 
+namespace detail {
+
+// The free functions below keep the engine of the catalog they saw last
+// (uploads, shard plans and device buffers are built once, like the Python
+// mirror's _evaluator_for): repeated calls on one catalog (benchmark_eval,
+// engine.hpp:280-285; cmd_loglik) pay only the evaluation.  The key is the
+// catalog's full content (64-bit FNV-1a over every event's t, lon, lat and
+// density bits, plus the size), so a different catalog at the same address
+// is never served a stale context.  Calls serialise on the cache's mutex.
+inline std::uint64_t catalog_fingerprint(const Catalog& catalog) {
+  std::uint64_t h = 1469598103934665603ULL;
+  auto mix = [&h](double v) {
+    std::uint64_t u;
+    std::memcpy(&u, &v, sizeof u);
+    for (int b = 0; b < 8; ++b) {
+      h ^= (u >> (8 * b)) & 0xffu;
+      h *= 1099511628211ULL;
+    }
+  };
+  for (std::size_t i = 0; i < catalog.size(); ++i) {
+    mix(catalog[i].t);
+    mix(catalog[i].lon);
+    mix(catalog[i].lat);
+    mix(catalog[i].density);
+  }
+  return h ^ catalog.size();
+}
+
+template <typename Fn>
+auto with_cached_engine(const Catalog& catalog, Fn&& fn) {
+  static std::mutex mu;
+  static std::unique_ptr<Engine> engine;
+  static std::uint64_t key = 0;
+  static std::size_t size = 0;
+  const std::uint64_t k = catalog_fingerprint(catalog);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!engine || k != key || size != catalog.size()) {
+    engine.reset();  // free the old context's device memory first
+    engine = std::make_unique<Engine>(catalog);
+    key = k;
+    size = catalog.size();
+  }
+  return fn(*engine);
+}
+
+}  // namespace detail
+
 /// engine.hpp:101-110 on the GPU (Precision::single: FP32 trigger arithmetic).
 inline double log_likelihood(const Catalog& catalog, const HawkesParams& p, const Partition& part,
                              Precision precision) {
   check_call(catalog, p, part);
-  Engine e(catalog);
-  return precision == Precision::dbl ? e.log_likelihood(p, p.variant)
-                                     : e.log_likelihood_single(p, p.variant);
+  return detail::with_cached_engine(catalog, [&](Engine& e) {
+    return precision == Precision::dbl ? e.log_likelihood(p, p.variant)
+                                       : e.log_likelihood_single(p, p.variant);
+  });
 }
 
 /// The log-likelihood and d ell / d (mu0, tau_t, xi0, sigma_x, sigma_t).
 inline double log_likelihood_and_gradient(const Catalog& catalog, const HawkesParams& p,
                                           const Partition& part, std::array<double, 5>& grad) {
   check_call(catalog, p, part);
-  return Engine(catalog).log_likelihood_and_gradient(p, p.variant, grad);
+  return detail::with_cached_engine(
+      catalog, [&](Engine& e) { return e.log_likelihood_and_gradient(p, p.variant, grad); });
 }
 
-/// model.hpp:351-356 on the GPU.
+/// model.hpp:225-230 on the GPU.
 inline double event_contribution(const HawkesParams& p, const Catalog& catalog, std::size_t n) {
   if (n >= catalog.size()) throw std::out_of_range("event_contribution: index out of range");
   p.validate();
-  return Engine(catalog).event_contribution(p, n);
+  return detail::with_cached_engine(catalog, [&](Engine& e) { return e.event_contribution(p, n); });
 }
 
 /// LikelihoodWorkspace<Real> (engine.hpp:117-229): same constructor and
@@ -167,18 +227,18 @@ class LikelihoodWorkspace {
   LikelihoodWorkspace(const Catalog& catalog, Variant variant, std::size_t /*workers*/)
       : engine_(catalog), variant_(variant) {}
 
-  // Real = float (Precision::single) evaluates through the FP32 trigger path
-  // without caching; Real = double uses the device-cached row sums.
+  // Real = double caches the FP64 row sums; Real = float (Precision::single)
+  // caches the same halves of the FP32-trigger arithmetic (hk_ws_eval_single).
   double evaluate_full(const HawkesParams& p) {
     current_ = p;
     return kDouble ? engine_.workspace_eval(p, variant_, /*force=*/true)
-                   : engine_.log_likelihood_single(p, variant_);
+                   : engine_.workspace_eval_single(p, variant_, /*force=*/true);
   }
 
   double evaluate_proposal(const HawkesParams& p) {
     proposal_ = p;
     return kDouble ? engine_.workspace_eval(p, variant_, /*force=*/false)
-                   : engine_.log_likelihood_single(p, variant_);
+                   : engine_.workspace_eval_single(p, variant_, /*force=*/false);
   }
 
   // Both the current and the proposal state stay cached on the device.

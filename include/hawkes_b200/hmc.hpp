@@ -88,6 +88,7 @@ class HmcSampler {
       engine_.set_locations(lon, lat);
     }
     value_ = log_density(z_, grad_);
+    loglik_ = last_ll_;
   }
 
   ChainOutput run() {
@@ -111,6 +112,7 @@ class HmcSampler {
         timing_.resample_wait += seconds(t0, t1);
         timing_.set_locations += seconds(t1, t2);
         value_ = log_density(z_, grad_);  // the target changed with X
+        loglik_ = last_ll_;  // a rejected transition keeps these locations' LL
       }
       const bool in_burn_in = iter < cfg_.chain.burn_in;
       const double accept_prob = transition();

@@ -53,6 +53,8 @@ class Oracle:
         L.orc_rows_ld.argtypes = [_dp, _dp, _dp, _dp, _sz, _dp, C.c_int, _up, _sz, _sz, _dp, C.c_void_p]
         L.orc_ll_grad.argtypes = [_dp, _dp, _dp, _dp, _sz, _dp, C.c_int, _sz, C.POINTER(C.c_double), _dp]
         L.orc_grad_scale.argtypes = [_dp, _dp, _dp, _dp, _sz, _dp, C.c_int, _sz, C.POINTER(C.c_double), _dp]
+        L.orc_ll_grad_dbl.argtypes = [_dp, _dp, _dp, _dp, _sz, _dp, C.c_int, _sz, C.POINTER(C.c_double),
+                                      _dp, _dp]
         L.orc_rows_lanes.argtypes = [_dp, _dp, _dp, _dp, _sz, _dp, C.c_int, _up, _sz, _sz, _dp]
         L.orc_integral_term.argtypes = [_dp, C.c_double, C.c_double]
         L.orc_integral_term.restype = C.c_double
@@ -100,6 +102,18 @@ class Oracle:
                                  C.byref(out), g):
             raise ValueError("orc_grad_scale: invalid arguments")
         return out.value, g
+
+    def ll_grad_dbl(self, cat, p, variant: int, threads: int = 0):
+        """Double-precision LL, gradient and conditioning scale (sum_n
+        |d ell_n / d theta|) with compensated row sums: the checker for
+        catalogs too large for the long-double path (N = 1e6)."""
+        t, x, y, d, n = self._cat(cat)
+        out = C.c_double()
+        g, sc = np.zeros(5), np.zeros(5)
+        if self.L.orc_ll_grad_dbl(t, x, y, d, n, _params(p), variant, threads or os.cpu_count() or 1,
+                                  C.byref(out), g, sc):
+            raise ValueError("orc_ll_grad_dbl: invalid arguments")
+        return out.value, g, sc
 
     def rows_ld(self, cat, p, variant: int, rows, threads: int = 0, grad: bool = True):
         t, x, y, d, n = self._cat(cat)
@@ -167,6 +181,7 @@ class Reference:
         L.ref_workspace_script.argtypes = [_dp, _dp, _dp, _dp, _sz, C.c_int, _sz,
                                            np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS"),
                                            _dp, _sz, _dp]
+        L.ref_county_densities.argtypes = [C.c_int, C.c_uint64, _dp]
         self.L = L
         self.path = path
 
@@ -179,6 +194,11 @@ class Reference:
         t, x, y, d = (np.zeros(n) for _ in range(4))
         self._check(self.L.ref_benchmark_catalog(n, seed, t, x, y, d))
         return t, x, y, d
+
+    def county_densities(self, grid: int = 60, seed: int = 1) -> np.ndarray:
+        out = np.zeros(grid * grid)
+        self._check(self.L.ref_county_densities(grid, seed, out))
+        return out
 
     def log_likelihood(self, cat, p, variant: int, workers: int = 1, single: bool = False) -> float:
         t, x, y, d = (_arr(a) for a in cat)
@@ -229,3 +249,14 @@ class Reference:
         out = np.zeros(len(ops))
         self._check(self.L.ref_workspace_script(t, x, y, d, len(t), variant, workers, ops, ps, len(ops), out))
         return out
+
+
+def county_index(x, y, grid: int = 60) -> np.ndarray:
+    """County of each event in BASELINE config 5's fixture:
+    grid x grid squares over [-5, 5]^2 in row-major order, the square
+    containing (x, y), clamped to the grid (tools/cpp/cut_posterior_bench.cpp
+    uses the same arithmetic: int((lon + 5) / (10 / grid)))."""
+    cell = 10.0 / grid
+    gx = np.minimum(((np.asarray(x) + 5.0) / cell).astype(np.int64), grid - 1)
+    gy = np.minimum(((np.asarray(y) + 5.0) / cell).astype(np.int64), grid - 1)
+    return gx + grid * gy

@@ -12,12 +12,14 @@
 //   benchmark_catalog          engine.hpp:251-259
 //   log_likelihood             engine.hpp:101-110  (Partition::make :27-40)
 //   slice_log_likelihood       engine.hpp:65-83
-//   event_contribution         model.hpp:351-356
+//   event_contribution         model.hpp:225-230
 //   naive_log_likelihood       simulate.hpp:121-136
-//   pair_rate / integral_term  model.hpp:360-376 / :301-306
+//   pair_rate / integral_term  model.hpp:234-250 / :301-306
 //   gaussian_pdf / gaussian_cdf model.hpp:27-34
 //   LikelihoodWorkspace<double> engine.hpp:117-229
+#include <cmath>
 #include <cstdint>
+#include <random>
 #include <cstring>
 #include <exception>
 #include <stdexcept>
@@ -162,6 +164,18 @@ int ref_integral_term(const double* params, double t_n, double t_end, double* ou
 
 double ref_gaussian_pdf(double z) { return gaussian_pdf(z); }
 double ref_gaussian_cdf(double z) { return gaussian_cdf(z); }
+
+// BASELINE config 5's county densities: grid x grid square
+// counties, densities log-uniform on [1, 7.4e4] drawn in row-major county
+// order from std::mt19937_64(seed) through std::uniform_real_distribution
+// (the same draws as tools/cpp/cut_posterior_bench.cpp).
+int ref_county_densities(int grid, std::uint64_t seed, double* out) {
+  return guarded([&] {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> ulog(0.0, std::log(7.4e4));
+    for (int k = 0; k < grid * grid; ++k) out[k] = std::exp(ulog(rng));
+  });
+}
 
 // Partition::make, flattened to n_workers+1 boundaries.
 int ref_partition(std::size_t n, std::size_t g, std::size_t* bounds) {

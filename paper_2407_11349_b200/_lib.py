@@ -44,13 +44,17 @@ _pp = C.POINTER(hk_params)
 SIGNATURES = [
     ("hk_create", C.c_int, [_dp, _dp, _dp, _dp, _sz, C.c_int, C.POINTER(_ctx)]),
     ("hk_create_variant", C.c_int, [_dp, _dp, _dp, _dp, _sz, C.c_int, C.c_int, C.POINTER(_ctx)]),
+    ("hk_create_devices", C.c_int, [_dp, _dp, _dp, _dp, _sz, np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS"),
+                                   C.c_int, C.c_int, C.POINTER(_ctx)]),
     ("hk_create_shard", C.c_int, [_dp, _dp, _dp, _dp, _sz, _sz, _sz, C.c_int, C.POINTER(_ctx)]),
     ("hk_destroy", None, [_ctx]),
     ("hk_set_locations", C.c_int, [_ctx, _dp, _dp]),
     ("hk_set_locations_device", C.c_int, [_ctx, C.c_void_p, C.c_void_p]),
     ("hk_eval", C.c_int, [_ctx, _pp, C.POINTER(C.c_double), C.c_void_p]),
+    ("hk_eval_detail", C.c_int, [_ctx, _pp, C.POINTER(C.c_double), C.c_void_p, C.c_void_p, C.c_void_p]),
     ("hk_eval_single", C.c_int, [_ctx, _pp, C.POINTER(C.c_double)]),
     ("hk_ws_eval", C.c_int, [_ctx, _pp, C.c_int, C.POINTER(C.c_double), C.c_void_p]),
+    ("hk_ws_eval_single", C.c_int, [_ctx, _pp, C.c_int, C.POINTER(C.c_double)]),
     ("hk_ws_stats", C.c_int, [_ctx, C.POINTER(C.c_long), C.POINTER(C.c_long)]),
     ("hk_eval_async", C.c_int, [_ctx, _pp, C.c_int]),
     ("hk_result_device", C.c_void_p, [_ctx]),
@@ -61,6 +65,7 @@ SIGNATURES = [
     ("hk_set_profiling", C.c_int, [_ctx, C.c_int]),
     ("hk_profile", C.c_int, [_ctx, C.POINTER(C.c_double), C.POINTER(C.c_long), C.POINTER(C.c_long)]),
     ("hk_reset_profile", C.c_int, [_ctx]),
+    ("hk_profile_kinds", C.c_int, [_ctx, _dp, np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")]),
     ("hk_validate_catalog", C.c_int, [_dp, _dp, _dp, _dp, _sz]),
     ("hk_validate_params", C.c_int, [_pp]),
     ("hk_partition_make", C.c_int, [_sz, _sz, _szp]),

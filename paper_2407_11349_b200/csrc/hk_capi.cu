@@ -7,9 +7,17 @@
 // uploaded once (hk_create) and locations replaced in place
 // (hk_set_locations), matching LikelihoodWorkspace's lifetime
 // (engine.hpp:117-229).  Multi-device contexts evaluate their shards
-// concurrently (one stream per device) and sum the per-device 6-vectors on
-// the host in device order, so the result is deterministic.
+// concurrently (one stream per device); the per-device 6-vectors
+// [ell, d ell / d theta] are all-gathered over NVLink with NCCL and summed
+// on the device in device order (deterministic), and new locations go to
+// device 0 once and are NCCL-broadcast to the others (north_star's data
+// plane; the reference's ordered slice reduction is engine.hpp:91-98).  A
+// context whose device list repeats a device (several shards on one GPU:
+// the single-GPU test of this path) moves the same bytes with peer copies
+// instead; the arithmetic is identical.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types and prototypes only: libnccl is dlopen'ed when a context needs it
 
 #include <algorithm>
 #include <cmath>
@@ -30,6 +38,45 @@ namespace {
 
 thread_local std::string g_err;
 
+// NCCL, loaded on first use by a multi-device context (the library itself
+// has no link-time NCCL dependency; in a PyTorch process this resolves to
+// the libnccl.so.2 torch already loaded).
+struct NcclApi {
+  decltype(&ncclCommInitAll) CommInitAll = nullptr;
+  decltype(&ncclCommDestroy) CommDestroy = nullptr;
+  decltype(&ncclAllGather) AllGather = nullptr;
+  decltype(&ncclBroadcast) Broadcast = nullptr;
+  decltype(&ncclGroupStart) GroupStart = nullptr;
+  decltype(&ncclGroupEnd) GroupEnd = nullptr;
+  decltype(&ncclGetErrorString) GetErrorString = nullptr;
+  std::string error;
+};
+
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      a.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+      return a;
+    }
+    auto sym = [&](auto& fp, const char* name) {
+      fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+      if (!fp && a.error.empty()) a.error = std::string("libnccl.so.2 lacks ") + name;
+    };
+    sym(a.CommInitAll, "ncclCommInitAll");
+    sym(a.CommDestroy, "ncclCommDestroy");
+    sym(a.AllGather, "ncclAllGather");
+    sym(a.Broadcast, "ncclBroadcast");
+    sym(a.GroupStart, "ncclGroupStart");
+    sym(a.GroupEnd, "ncclGroupEnd");
+    sym(a.GetErrorString, "ncclGetErrorString");
+    return a;
+  }();
+  return api;
+}
+
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -39,6 +86,10 @@ struct NotImplemented : std::runtime_error {
 
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw CudaError(std::string(what) + ": " + nccl_api().GetErrorString(r));
 }
 
 template <typename Fn>
@@ -114,7 +165,11 @@ struct DeviceState {
   int n_finish_blocks = 0;
   double* out6 = nullptr;
   double* h_out6 = nullptr;  // pinned
+  double* gather6 = nullptr;  // [n_dev][6]: every device's out6 (multi-device contexts)
+  double* total6 = nullptr;   // their device-order sum
+  cudaEvent_t done = nullptr; // peer-copy mode: this device's part is ready
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  std::vector<int> prof_kind;  // per used event pair: 0 both halves, 1 background, 2 trigger
   std::size_t prof_used = 0;
 
   hk::DeviceCatalog catalog(int n, int npad) const {
@@ -133,6 +188,13 @@ struct hk_ctx {
   bool unit_density = false;  // every density == 1: varying == constant exactly
   bool locations_valid = true;  // false for a coarse-only catalog until set_locations
   std::vector<DeviceState> devs;
+  // multi-device data plane: NCCL communicators over distinct devices, or
+  // peer copies when the device list repeats a device
+  bool use_nccl = false;
+  std::vector<ncclComm_t> comms;
+  double* bbox_scratch = nullptr;  // device 0
+  double* bbox_out = nullptr;      // device 0, 5 doubles
+  double* h_bbox = nullptr;        // pinned
   bool profiling = false;
   int bg_expansion = 1;
 
@@ -157,6 +219,14 @@ struct hk_ctx {
   long prof_pair = 0, prof_total = 0;
 
   ~hk_ctx() {
+    for (ncclComm_t c : comms)
+      if (c) nccl_api().CommDestroy(c);
+    if (!devs.empty()) {
+      cudaSetDevice(devs[0].dev);
+      if (bbox_scratch) cudaFree(bbox_scratch);
+      if (bbox_out) cudaFree(bbox_out);
+      if (h_bbox) cudaFreeHost(h_bbox);
+    }
     for (auto& s : devs) {
       cudaSetDevice(s.dev);
       if (s.stream) cudaStreamSynchronize(s.stream);
@@ -173,6 +243,9 @@ struct hk_ctx {
       for (hk::Item* it : s.items)
         if (it) cudaFree(it);
       if (s.h_out6) cudaFreeHost(s.h_out6);
+      if (s.gather6) cudaFree(s.gather6);
+      if (s.total6) cudaFree(s.total6);
+      if (s.done) cudaEventDestroy(s.done);
       for (auto& e : s.prof_events) {
         cudaEventDestroy(e.first);
         cudaEventDestroy(e.second);
@@ -181,15 +254,28 @@ struct hk_ctx {
     }
   }
 
-  void update_bbox() {
-    locations_valid = true;
-    for (int i = 0; i < n && locations_valid; ++i)
-      locations_valid = std::isfinite(x[i]) && std::isfinite(y[i]);
+  // The evaluation frame from the locations' box (argument bound of the
+  // exp mode, FP32 culling frame); `bad` = first non-finite index or n.
+  void set_bbox(double xmin, double xmax, double ymin, double ymax, long bad) {
+    locations_valid = bad >= n;
     if (!locations_valid) {
       d2_max = 0.0;
       cx = cy = half_extent = 0.0;
       return;
     }
+    const double w = xmax - xmin, h = ymax - ymin;
+    d2_max = w * w + h * h;
+    cx = 0.5 * (xmin + xmax);
+    cy = 0.5 * (ymin + ymax);
+    half_extent = 0.5 * std::max(w, h);
+  }
+
+  // host version (hk_create, before any device exists)
+  void update_bbox() {
+    long bad = n;
+    for (int i = 0; i < n && bad == n; ++i)
+      if (!std::isfinite(x[i]) || !std::isfinite(y[i])) bad = i;
+    if (bad < n) return set_bbox(0, 0, 0, 0, bad);
     double xmin = x[0], xmax = x[0], ymin = y[0], ymax = y[0];
     for (int i = 1; i < n; ++i) {
       xmin = std::min(xmin, x[i]);
@@ -197,11 +283,81 @@ struct hk_ctx {
       ymin = std::min(ymin, y[i]);
       ymax = std::max(ymax, y[i]);
     }
-    const double w = xmax - xmin, h = ymax - ymin;
-    d2_max = w * w + h * h;
-    cx = 0.5 * (xmin + xmax);
-    cy = 0.5 * (ymin + ymax);
-    half_extent = 0.5 * std::max(w, h);
+    set_bbox(xmin, xmax, ymin, ymax, n);
+  }
+
+  // Multi-device set-up after every device is initialised: NCCL
+  // communicators over distinct devices (HK_NO_NCCL=1 or a repeated device:
+  // peer copies), the gather buffers, and device 0's bbox buffers.
+  void init_data_plane() {
+    const int g = static_cast<int>(devs.size());
+    ck(cudaSetDevice(devs[0].dev), "cudaSetDevice");
+    bbox_scratch = dmalloc<double>(hk::bbox_scratch_doubles());
+    bbox_out = dmalloc<double>(5);
+    ck(cudaMallocHost(&h_bbox, 5 * sizeof(double)), "cudaMallocHost");
+    if (g == 1) return;
+    std::vector<int> ids(g);
+    for (int k = 0; k < g; ++k) ids[k] = devs[k].dev;
+    std::vector<int> sorted_ids = ids;
+    std::sort(sorted_ids.begin(), sorted_ids.end());
+    const bool distinct = std::adjacent_find(sorted_ids.begin(), sorted_ids.end()) == sorted_ids.end();
+    const char* no = std::getenv("HK_NO_NCCL");
+    use_nccl = distinct && !(no && std::atoi(no) != 0);
+    for (auto& s : devs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      s.gather6 = dmalloc<double>(6 * static_cast<std::size_t>(g));
+      s.total6 = dmalloc<double>(6);
+      ck(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "cudaEventCreate");
+    }
+    if (use_nccl) {
+      const NcclApi& api = nccl_api();
+      if (!api.error.empty())
+        throw CudaError("multi-device context needs NCCL: " + api.error +
+                        " (HK_NO_NCCL=1 moves the 6-vectors and locations with peer copies instead)");
+      comms.assign(g, nullptr);
+      nck(api.CommInitAll(comms.data(), g, ids.data()), "ncclCommInitAll");
+    }
+  }
+
+  // Device 0's x, y (already written) -> box + finiteness check on device 0
+  // -> NCCL broadcast (or peer copies) to the other devices.  Throws the
+  // reference's Catalog message for a non-finite location.
+  void publish_locations() {
+    DeviceState& s0 = devs[0];
+    ck(cudaSetDevice(s0.dev), "cudaSetDevice");
+    hk::launch_bbox(s0.x, s0.y, n, bbox_scratch, bbox_out, s0.stream);
+    ck(cudaMemcpyAsync(h_bbox, bbox_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, s0.stream),
+       "bbox copy");
+    const int g = static_cast<int>(devs.size());
+    if (g > 1) {
+      if (use_nccl) {
+        const NcclApi& api = nccl_api();
+        nck(api.GroupStart(), "ncclGroupStart");
+        for (int k = 0; k < g; ++k) {
+          DeviceState& s = devs[k];
+          ck(cudaSetDevice(s.dev), "cudaSetDevice");
+          nck(api.Broadcast(s0.x, s.x, n, ncclFloat64, 0, comms[k], s.stream), "ncclBroadcast");
+          nck(api.Broadcast(s0.y, s.y, n, ncclFloat64, 0, comms[k], s.stream), "ncclBroadcast");
+        }
+        nck(api.GroupEnd(), "ncclGroupEnd");
+      } else {
+        ck(cudaEventRecord(s0.done, s0.stream), "cudaEventRecord");
+        for (int k = 1; k < g; ++k) {
+          DeviceState& s = devs[k];
+          ck(cudaSetDevice(s.dev), "cudaSetDevice");
+          ck(cudaStreamWaitEvent(s.stream, s0.done, 0), "cudaStreamWaitEvent");
+          ck(cudaMemcpyPeerAsync(s.x, s.dev, s0.x, s0.dev, n * sizeof(double), s.stream), "peer copy");
+          ck(cudaMemcpyPeerAsync(s.y, s.dev, s0.y, s0.dev, n * sizeof(double), s.stream), "peer copy");
+        }
+      }
+    }
+    ck(cudaSetDevice(s0.dev), "cudaSetDevice");
+    ck(cudaStreamSynchronize(s0.stream), "set_locations");
+    set_bbox(h_bbox[0], h_bbox[1], h_bbox[2], h_bbox[3], static_cast<long>(h_bbox[4]));
+    ++loc_version;  // drops the trigger caches (engine.hpp:177)
+    if (!locations_valid)
+      throw std::invalid_argument("Catalog: event " + std::to_string(static_cast<long>(h_bbox[4])) +
+                                  " has non-finite location");
   }
 
   void upload_padded(DeviceState& s, double* dst, const std::vector<double>& src, double pad) {
@@ -273,14 +429,28 @@ struct hk_ctx {
     ck(cudaMallocHost(&s.h_out6, 6 * sizeof(double)), "cudaMallocHost");
   }
 
-  std::pair<cudaEvent_t, cudaEvent_t> next_events(DeviceState& s) {
+  std::pair<cudaEvent_t, cudaEvent_t> next_events(DeviceState& s, int kind) {
     if (s.prof_used == s.prof_events.size()) {
       cudaEvent_t a, b;
       ck(cudaEventCreate(&a), "cudaEventCreate");
       ck(cudaEventCreate(&b), "cudaEventCreate");
       s.prof_events.emplace_back(a, b);
+      s.prof_kind.push_back(0);
     }
+    s.prof_kind[s.prof_used] = kind;
     return s.prof_events[s.prof_used++];
+  }
+
+  // One pair launch, bracketed by profiling events of its kind when enabled.
+  template <typename Fn>
+  void timed_pair(DeviceState& s, int kind, Fn&& launch) {
+    std::pair<cudaEvent_t, cudaEvent_t> ev{};
+    if (profiling) {
+      ev = next_events(s, kind);
+      ck(cudaEventRecord(ev.first, s.stream), "cudaEventRecord");
+    }
+    launch();
+    if (profiling) ck(cudaEventRecord(ev.second, s.stream), "cudaEventRecord");
   }
 
   hk::EvalCoef coef(const hk_params* p, bool single = false) const {
@@ -313,8 +483,12 @@ struct hk_ctx {
   // recently used entry, which the next enqueue recomputes.  Returns the
   // halves to compute.
   int plan_halves(const hk::EvalCoef& c, bool grad, bool force, int& bgi, int& tri) {
+    // the background half is FP64 in both precisions, but each precision
+    // keeps its own entries so a cached result is bitwise the fresh one of
+    // the same precision (the launches differ between the two)
     auto hit_bg = [&](const Key& k) {
-      return k.valid && k.a == c.tau_t && k.bgx == c.bg_expansion && (k.grad || !grad);
+      return k.valid && k.a == c.tau_t && k.b == c.single_prec && k.bgx == c.bg_expansion &&
+             (k.grad || !grad);
     };
     auto hit_tr = [&](const Key& k) {
       return k.valid && k.a == c.sigma_x && k.b == c.sigma_t && k.variant == tr_variant(c) &&
@@ -331,7 +505,8 @@ struct hk_ctx {
     if (bgi < 0) {
       halves |= hk::kHalfBg;
       bgi = bg_key[0].used <= bg_key[1].used ? 0 : 1;
-      bg_key[bgi] = Key{true, c.tau_t, 0, 0, grad ? 1 : 0, c.bg_expansion, 0, 0};
+      bg_key[bgi] = Key{true, c.tau_t, static_cast<double>(c.single_prec), 0, grad ? 1 : 0,
+                        c.bg_expansion, 0, 0};
     }
     if (tri < 0) {
       halves |= hk::kHalfTr;
@@ -345,7 +520,10 @@ struct hk_ctx {
   }
 
   // Enqueues [prep + pair + collapse for the missing halves] + finish + reduce.
-  void enqueue(DeviceState& s, const hk::EvalCoef& c, bool grad, int halves, int bgi, int tri) {
+  // ell_rows / grad_rows (device, optional): the shard's per-row ell_n and
+  // d ell_n / d theta from the same launches.
+  void enqueue(DeviceState& s, const hk::EvalCoef& c, bool grad, int halves, int bgi, int tri,
+               double* ell_rows = nullptr, double* grad_rows = nullptr) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const hk::DeviceCatalog dc = s.catalog(n, npad);
     const int rows = s.re - s.rb;
@@ -359,11 +537,6 @@ struct hk_ctx {
     }
     if (halves) {
       hk::launch_prep(dc, c, s.stream);
-      std::pair<cudaEvent_t, cudaEvent_t> ev{};
-      if (profiling) {
-        ev = next_events(s);
-        ck(cudaEventRecord(ev.first, s.stream), "cudaEventRecord");
-      }
       const int v = c.varying ? 1 : 0;
       // The density-scaled kernel's rows come in clustered windows that span
       // far more time than a row block, which would disqualify the
@@ -378,15 +551,21 @@ struct hk_ctx {
         hk::EvalCoef cb = c;
         cb.varying = 0;
         if (halves & hk::kHalfBg)
-          hk::launch_pair(dc, cb, s.items[0], s.n_items[0], s.partial, s.rb, rows, grad, hk::kHalfBg,
-                          s.stream);
+          timed_pair(s, 1, [&] {
+            hk::launch_pair(dc, cb, s.items[0], s.n_items[0], s.partial, s.rb, rows, grad, hk::kHalfBg,
+                            s.stream);
+          });
         if (halves & hk::kHalfTr)
-          hk::launch_pair(dc, c, s.items[1], s.n_items[1], s.partial, s.rb, rows, grad, hk::kHalfTr,
-                          s.stream);
+          timed_pair(s, 2, [&] {
+            hk::launch_pair(dc, c, s.items[1], s.n_items[1], s.partial, s.rb, rows, grad, hk::kHalfTr,
+                            s.stream);
+          });
       } else {
-        hk::launch_pair(dc, c, s.items[v], s.n_items[v], s.partial, s.rb, rows, grad, halves, s.stream);
+        const int kind = halves == (hk::kHalfBg | hk::kHalfTr) ? 0 : (halves == hk::kHalfBg ? 1 : 2);
+        timed_pair(s, kind, [&] {
+          hk::launch_pair(dc, c, s.items[v], s.n_items[v], s.partial, s.rb, rows, grad, halves, s.stream);
+        });
       }
-      if (profiling) ck(cudaEventRecord(ev.second, s.stream), "cudaEventRecord");
       if (split) {
         if (halves & hk::kHalfBg)
           hk::launch_collapse(s.partial, s.slots[0], rows, s.bg_sums[bgi], nullptr, s.stream);
@@ -401,34 +580,107 @@ struct hk_ctx {
       }
       if (profiling) prof_pair += 1;
     }
-    hk::launch_finish(dc, c, s.bg_sums[bgi], s.tr_sums[tri], s.rb, rows, grad, nullptr, nullptr,
-                      s.blockpart, s.stream);
+    hk::launch_finish(dc, c, s.bg_sums[bgi], s.tr_sums[tri], s.rb, rows, grad, ell_rows,
+                      grad ? grad_rows : nullptr, s.blockpart, s.stream);
     hk::launch_reduce(s.blockpart, s.n_finish_blocks, s.out6, s.stream);
     ck(cudaGetLastError(), "kernel launch");
     prof_total += 2;
   }
 
   // Full or workspace evaluation on every device; sums in device order.
+  // ell_rows / grad_rows (host, optional): per-row outputs of the context's
+  // rows, devices in order (hk_eval_detail).
   void evaluate(const hk_params* p, bool grad, bool workspace, bool force, double* ll, double* grad5,
-                bool single = false) {
+                bool single = false, double* ell_rows = nullptr, double* grad_rows = nullptr) {
     const hk::EvalCoef c = coef(p, single);
     int bgi, tri;
     const int halves = workspace ? plan_halves(c, grad, force, bgi, tri)
                                  : plan_halves(c, grad, /*force=*/true, bgi, tri);
-    for (auto& s : devs) {
-      enqueue(s, c, grad, halves, bgi, tri);
-      ck(cudaMemcpyAsync(s.h_out6, s.out6, 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
+    std::vector<double*> dev_rows(devs.size(), nullptr);
+    struct Free {
+      std::vector<double*>& v;
+      ~Free() {
+        for (double* q : v)
+          if (q) cudaFree(q);
+      }
+    } free_rows{dev_rows};
+    std::size_t off = 0;
+    for (std::size_t k = 0; k < devs.size(); ++k) {
+      auto& s = devs[k];
+      const std::size_t rows = static_cast<std::size_t>(s.re - s.rb);
+      double *d_ell = nullptr, *d_grad = nullptr;
+      if (ell_rows || grad_rows) {
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        dev_rows[k] = dmalloc<double>(6 * rows);
+        d_ell = dev_rows[k];
+        d_grad = dev_rows[k] + rows;
+      }
+      enqueue(s, c, grad, halves, bgi, tri, d_ell, d_grad);
+      if (devs.size() == 1)
+        ck(cudaMemcpyAsync(s.h_out6, s.out6, 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
+           "result copy");
+      if (ell_rows)
+        ck(cudaMemcpyAsync(ell_rows + off, d_ell, rows * sizeof(double), cudaMemcpyDeviceToHost,
+                           s.stream),
+           "rows copy");
+      if (grad_rows && grad)
+        ck(cudaMemcpyAsync(grad_rows + 5 * off, d_grad, 5 * rows * sizeof(double),
+                           cudaMemcpyDeviceToHost, s.stream),
+           "rows copy");
+      off += rows;
+    }
+    if (devs.size() > 1) {
+      reduce_devices();
+      ck(cudaSetDevice(devs[0].dev), "cudaSetDevice");
+      ck(cudaMemcpyAsync(devs[0].h_out6, devs[0].total6, 6 * sizeof(double), cudaMemcpyDeviceToHost,
+                         devs[0].stream),
          "result copy");
     }
-    double acc[6] = {0, 0, 0, 0, 0, 0};
-    for (auto& s : devs) {  // device order: deterministic
+    for (auto& s : devs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       ck(cudaStreamSynchronize(s.stream), "hk_eval");
-      for (int k = 0; k < 6; ++k) acc[k] += s.h_out6[k];
     }
+    const double* acc = devs[0].h_out6;
     *ll = acc[0];
     if (grad5)
       for (int k = 0; k < 5; ++k) grad5[k] = acc[1 + k];
+  }
+
+  // The per-device 6-vectors -> their device-order sum in total6: an NCCL
+  // all-gather of 6 doubles per device (every device then holds the total),
+  // or peer copies into device 0.  Enqueued, not synchronised.
+  void reduce_devices() {
+    const int g = static_cast<int>(devs.size());
+    if (use_nccl) {
+      const NcclApi& api = nccl_api();
+      nck(api.GroupStart(), "ncclGroupStart");
+      for (int k = 0; k < g; ++k) {
+        DeviceState& s = devs[k];
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        nck(api.AllGather(s.out6, s.gather6, 6, ncclFloat64, comms[k], s.stream), "ncclAllGather");
+      }
+      nck(api.GroupEnd(), "ncclGroupEnd");
+      for (auto& s : devs) {
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        hk::launch_sum6(s.gather6, g, s.total6, s.stream);
+      }
+    } else {
+      for (auto& s : devs) {
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        ck(cudaEventRecord(s.done, s.stream), "cudaEventRecord");
+      }
+      DeviceState& s0 = devs[0];
+      ck(cudaSetDevice(s0.dev), "cudaSetDevice");
+      for (int k = 0; k < g; ++k) {
+        ck(cudaStreamWaitEvent(s0.stream, devs[k].done, 0), "cudaStreamWaitEvent");
+        ck(cudaMemcpyPeerAsync(s0.gather6 + 6 * k, s0.dev, devs[k].out6, devs[k].dev, 6 * sizeof(double),
+                               s0.stream),
+           "peer copy");
+      }
+      hk::launch_sum6(s0.gather6, g, s0.total6, s0.stream);
+    }
+    ck(cudaGetLastError(), "sum6");
+    prof_total += use_nccl ? g : 1;
   }
 };
 
@@ -467,8 +719,12 @@ int hk_create(const double* t, const double* lon, const double* lat, const doubl
   return hk_create_variant(t, lon, lat, density, n, n_gpus, HK_VARIANT_CONSTANT, out);
 }
 
-int hk_create_variant(const double* t, const double* lon, const double* lat, const double* density,
-                      size_t n, int n_gpus, int variant, hk_ctx** out) {
+namespace {
+
+// A context over an explicit device list: cost-balanced row shards, one per
+// entry (shard k on devices[k]), then the multi-device data plane.
+int create_on(const double* t, const double* lon, const double* lat, const double* density, size_t n,
+              const int* devices, int n_dev, int variant, hk_ctx** out) {
   return guarded([&] {
     if (!out) throw std::invalid_argument("hk_create: null output");
     if (variant != HK_VARIANT_CONSTANT && variant != HK_VARIANT_VARYING)
@@ -477,20 +733,43 @@ int hk_create_variant(const double* t, const double* lon, const double* lat, con
     auto ctx = new_ctx(t, lon, lat, density, n);
     int avail = 0;
     ck(cudaGetDeviceCount(&avail), "cudaGetDeviceCount");
-    const int g = n_gpus <= 0 ? 1 : n_gpus;
-    if (g > avail)
-      throw std::invalid_argument("hk_create: requested " + std::to_string(g) +
-                                  " GPUs, " + std::to_string(avail) + " visible");
-    if (static_cast<std::size_t>(g) > n) throw std::invalid_argument("Partition: more workers than terms");
+    const int top = *std::max_element(devices, devices + n_dev);
+    if (top >= avail)
+      throw std::invalid_argument("hk_create: requested " + std::to_string(top + 1) + " GPUs, " +
+                                  std::to_string(avail) + " visible");
+    if (*std::min_element(devices, devices + n_dev) < 0)
+      throw std::invalid_argument("hk_create: negative device index");
+    if (static_cast<std::size_t>(n_dev) > n) throw std::invalid_argument("Partition: more workers than terms");
     const double beta = variant == HK_VARIANT_VARYING ? hk::kCostBetaVarying
                         : n >= hk::kExpansionRows        ? hk::kCostBetaExpanded
                                                          : hk::kCostBeta;
-    const auto bounds = hk::plan_shards(ctx->lb, static_cast<std::size_t>(g), beta);
-    ctx->devs.resize(g);
-    for (int i = 0; i < g; ++i)
-      ctx->init_device(ctx->devs[i], i, static_cast<int>(bounds[i]), static_cast<int>(bounds[i + 1]));
+    const auto bounds = hk::plan_shards(ctx->lb, static_cast<std::size_t>(n_dev), beta);
+    ctx->devs.resize(n_dev);
+    for (int i = 0; i < n_dev; ++i)
+      ctx->init_device(ctx->devs[i], devices[i], static_cast<int>(bounds[i]), static_cast<int>(bounds[i + 1]));
+    ctx->init_data_plane();
     *out = ctx.release();
   });
+}
+
+}  // namespace
+
+int hk_create_variant(const double* t, const double* lon, const double* lat, const double* density,
+                      size_t n, int n_gpus, int variant, hk_ctx** out) {
+  const int g = n_gpus <= 0 ? 1 : n_gpus;
+  std::vector<int> devices(g);
+  for (int k = 0; k < g; ++k) devices[k] = k;
+  return create_on(t, lon, lat, density, n, devices.data(), g, variant, out);
+}
+
+int hk_create_devices(const double* t, const double* lon, const double* lat, const double* density,
+                      size_t n, const int* devices, int n_devices, int variant, hk_ctx** out) {
+  if (!devices || n_devices <= 0) {
+    g_err = "hk_create_devices: empty device list";
+    if (out) *out = nullptr;
+    return HK_INVALID_ARGUMENT;
+  }
+  return create_on(t, lon, lat, density, n, devices, n_devices, variant, out);
 }
 
 int hk_create_shard(const double* t, const double* lon, const double* lat, const double* density,
@@ -506,6 +785,7 @@ int hk_create_shard(const double* t, const double* lon, const double* lat, const
     if (device < 0 || device >= avail) throw std::invalid_argument("hk_create_shard: bad device");
     ctx->devs.resize(1);
     ctx->init_device(ctx->devs[0], device, static_cast<int>(row_begin), static_cast<int>(row_end));
+    ctx->init_data_plane();
     *out = ctx.release();
   });
 }
@@ -515,21 +795,15 @@ void hk_destroy(hk_ctx* ctx) { delete ctx; }
 int hk_set_locations(hk_ctx* ctx, const double* lon, const double* lat) {
   return guarded([&] {
     if (!ctx || !lon || !lat) throw std::invalid_argument("hk_set_locations: null argument");
-    for (int i = 0; i < ctx->n; ++i)
-      if (!std::isfinite(lon[i]) || !std::isfinite(lat[i]))
-        throw std::invalid_argument("Catalog: event " + std::to_string(i) +
-                                    " has non-finite location");
-    std::copy(lon, lon + ctx->n, ctx->x.begin());
-    std::copy(lat, lat + ctx->n, ctx->y.begin());
-    ctx->update_bbox();
-    ++ctx->loc_version;  // drops the trigger caches (engine.hpp:177)
-    for (auto& s : ctx->devs) {
-      ck(cudaSetDevice(s.dev), "cudaSetDevice");
-      ck(cudaMemcpyAsync(s.x, lon, ctx->n * sizeof(double), cudaMemcpyHostToDevice, s.stream),
-         "set_locations");
-      ck(cudaMemcpyAsync(s.y, lat, ctx->n * sizeof(double), cudaMemcpyHostToDevice, s.stream),
-         "set_locations");
-    }
+    auto& s0 = ctx->devs[0];
+    ck(cudaSetDevice(s0.dev), "cudaSetDevice");
+    // one host->device copy (asynchronous from pinned memory), then the box
+    // check on device 0 and the NCCL broadcast to the other devices
+    ck(cudaMemcpyAsync(s0.x, lon, ctx->n * sizeof(double), cudaMemcpyHostToDevice, s0.stream),
+       "set_locations");
+    ck(cudaMemcpyAsync(s0.y, lat, ctx->n * sizeof(double), cudaMemcpyHostToDevice, s0.stream),
+       "set_locations");
+    ctx->publish_locations();
   });
 }
 
@@ -537,24 +811,13 @@ int hk_set_locations_device(hk_ctx* ctx, const double* lon_device, const double*
   return guarded([&] {
     if (!ctx || !lon_device || !lat_device)
       throw std::invalid_argument("hk_set_locations_device: null argument");
-    if (ctx->devs.size() != 1)
-      throw std::invalid_argument("hk_set_locations_device: single-device contexts only");
     auto& s = ctx->devs[0];
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     ck(cudaMemcpyAsync(s.x, lon_device, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, s.stream),
        "set_locations_device");
     ck(cudaMemcpyAsync(s.y, lat_device, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, s.stream),
        "set_locations_device");
-    // Host mirror for the argument bound (bbox) and hk_eval_rows.
-    ck(cudaMemcpyAsync(ctx->x.data(), lon_device, ctx->n * sizeof(double), cudaMemcpyDeviceToHost,
-                       s.stream),
-       "mirror");
-    ck(cudaMemcpyAsync(ctx->y.data(), lat_device, ctx->n * sizeof(double), cudaMemcpyDeviceToHost,
-                       s.stream),
-       "mirror");
-    ck(cudaStreamSynchronize(s.stream), "mirror sync");
-    ctx->update_bbox();
-    ++ctx->loc_version;
+    ctx->publish_locations();
   });
 }
 
@@ -562,6 +825,17 @@ int hk_eval(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5) {
   return guarded([&] {
     if (!ctx || !ll) throw std::invalid_argument("hk_eval: null argument");
     ctx->evaluate(p, grad5 != nullptr, /*workspace=*/false, /*force=*/true, ll, grad5);
+  });
+}
+
+int hk_eval_detail(hk_ctx* ctx, const hk_params* p, double* ll, double* grad5, double* ell_rows,
+                   double* grad_rows) {
+  return guarded([&] {
+    if (!ctx || !ll) throw std::invalid_argument("hk_eval_detail: null argument");
+    if (grad_rows && !grad5)
+      throw std::invalid_argument("hk_eval_detail: grad_rows needs grad5");
+    ctx->evaluate(p, grad5 != nullptr, /*workspace=*/false, /*force=*/true, ll, grad5,
+                  /*single=*/false, ell_rows, grad_rows);
   });
 }
 
@@ -579,6 +853,13 @@ int hk_ws_eval(hk_ctx* ctx, const hk_params* p, int force, double* ll, double* g
   });
 }
 
+int hk_ws_eval_single(hk_ctx* ctx, const hk_params* p, int force, double* ll) {
+  return guarded([&] {
+    if (!ctx || !ll) throw std::invalid_argument("hk_ws_eval_single: null argument");
+    ctx->evaluate(p, /*grad=*/false, /*workspace=*/true, force != 0, ll, nullptr, /*single=*/true);
+  });
+}
+
 int hk_ws_stats(const hk_ctx* ctx, long* hits, long* misses) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("hk_ws_stats: null context");
@@ -590,17 +871,17 @@ int hk_ws_stats(const hk_ctx* ctx, long* hits, long* misses) {
 int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("hk_eval_async: null context");
-    if (ctx->devs.size() != 1)
-      throw std::invalid_argument("hk_eval_async: single-device contexts only");
     const hk::EvalCoef c = ctx->coef(p);
     int bgi, tri;
     const int halves = ctx->plan_halves(c, with_grad != 0, /*force=*/true, bgi, tri);
-    ctx->enqueue(ctx->devs[0], c, with_grad != 0, halves, bgi, tri);
+    for (auto& s : ctx->devs) ctx->enqueue(s, c, with_grad != 0, halves, bgi, tri);
+    if (ctx->devs.size() > 1) ctx->reduce_devices();
   });
 }
 
 const double* hk_result_device(hk_ctx* ctx) {
-  return (ctx && !ctx->devs.empty()) ? ctx->devs[0].out6 : nullptr;
+  if (!ctx || ctx->devs.empty()) return nullptr;
+  return ctx->devs.size() > 1 ? ctx->devs[0].total6 : ctx->devs[0].out6;
 }
 
 void* hk_stream(hk_ctx* ctx, int dev) {
@@ -712,6 +993,27 @@ int hk_profile(hk_ctx* ctx, double* pair_kernel_ms, long* pair_launches, long* t
     if (pair_kernel_ms) *pair_kernel_ms = ms;
     if (pair_launches) *pair_launches = ctx->prof_pair;
     if (total_launches) *total_launches = ctx->prof_total;
+  });
+}
+
+int hk_profile_kinds(hk_ctx* ctx, double* ms3, long* launches3) {
+  return guarded([&] {
+    if (!ctx || !ms3 || !launches3) throw std::invalid_argument("hk_profile_kinds: null argument");
+    for (int k = 0; k < 3; ++k) {
+      ms3[k] = 0.0;
+      launches3[k] = 0;
+    }
+    for (auto& s : ctx->devs) {
+      ck(cudaSetDevice(s.dev), "cudaSetDevice");
+      ck(cudaStreamSynchronize(s.stream), "hk_profile_kinds");
+      for (std::size_t i = 0; i < s.prof_used; ++i) {
+        float m = 0.f;
+        ck(cudaEventElapsedTime(&m, s.prof_events[i].first, s.prof_events[i].second),
+           "cudaEventElapsedTime");
+        ms3[s.prof_kind[i]] += m;
+        launches3[s.prof_kind[i]] += 1;
+      }
+    }
   });
 }
 

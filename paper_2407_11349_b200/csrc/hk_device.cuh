@@ -1,7 +1,7 @@
 // Device-side constants and the FP64 exponential used inside the pair loops.
 //
 // The reference evaluates every pair term with libm `exp`
-// (model.hpp:181 `detail::exp_nonpos`).  There is no FP64 MUFU on B200, so
+// (model.hpp:55 `detail::exp_nonpos`).  There is no FP64 MUFU on B200, so
 // exp is a DFMA polynomial and it dominates the FP64 pipe.  This exp works in
 // units of ln2/kTab: the caller folds the kTab/ln2 factor into the per-
 // evaluation coefficient K, so the range reduction is fused with the
@@ -28,7 +28,7 @@
 //   kExact   |x*K| < 1020 kTab for every evaluated term: no flush/validity test.
 //   kFlush   |x*K| < 2^30: results below 2^-1021 flush to +0 (the reference
 //            keeps subnormals; the difference is < 2.3e-308 absolute, far
-//            under the 1e-40 rate clip of model.hpp:144).
+//            under the 1e-40 rate clip of model.hpp:18).
 //   kChecked anything else: also rejects arguments whose k left int32.
 #pragma once
 
@@ -80,9 +80,9 @@ constexpr int kTabBits = HK_TAB_BITS;              // table of 2^(j/kTab), j < k
 constexpr int kTab = 1 << kTabBits;
 
 constexpr double kMagic = 6755399441055744.0;      // 1.5 * 2^52
-constexpr double kRateClip = 1e-40;                // model.hpp:144
-constexpr double kInvSqrt2Pi = 0.3989422804014327;  // model.hpp:149
-constexpr double kInv2Pi = 0.15915494309189535;     // model.hpp:150
+constexpr double kRateClip = 1e-40;                // model.hpp:18
+constexpr double kInvSqrt2Pi = 0.3989422804014327;  // model.hpp:23
+constexpr double kInv2Pi = 0.15915494309189535;     // model.hpp:24
 // Argument bounds in units of ln2/kTab: below kExactArg no term can leave
 // the normal range (|k >> kTabBits| < 1021); beyond kFlushArg every term
 // flushes to 0; below kCheckArg k stays far inside int32.

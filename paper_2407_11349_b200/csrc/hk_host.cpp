@@ -2,6 +2,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -176,11 +177,16 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
   const int ntiles = npad / kBJ;
   const int nblocks = (re - rb + kBI - 1) / kBI;
   const int G = std::max(1, window);
-  // Enough items to keep every SM busy for many waves (148 SMs x 4 CTAs x
-  // 16) and none larger than ~2^25 pair terms, capped at one tile each.
-  const double pairs_per_block = static_cast<double>(std::min(kBI, re - rb)) * n;
-  int slots = static_cast<int>(std::ceil(pairs_per_block / double(1 << 25)));
-  slots = std::max(slots, (148 * 4 * 16 + nblocks - 1) / nblocks);
+  // Column chunks per row block ("slots"): about kItemTarget work items
+  // (heaviest first, so the tail stays short), at most kMaxSlots, and chunks
+  // of at most kMaxItemTiles tiles (the kernel classifies an item's tiles in
+  // shared memory).  The partial-sum buffer [slots][5][rows] (40 B per row
+  // and slot) is therefore O(N) with a bounded constant: 17 slots at
+  // N = 1e6 (0.68 GB), 20 at N = 1e7 (8 GB).  HK_ITEM_TARGET overrides the
+  // item target (tuning).
+  int target = kItemTarget;
+  if (const char* e = std::getenv("HK_ITEM_TARGET")) target = std::max(1, std::atoi(e));
+  int slots = std::min(kMaxSlots, (target + nblocks - 1) / nblocks);
   slots = std::max(slots, (ntiles + kMaxItemTiles - 1) / kMaxItemTiles);
   slots = std::max(1, std::min(slots, ntiles));
   const int per = (ntiles + slots - 1) / slots;
@@ -234,9 +240,9 @@ EvalCoef make_coef(const ParamsIn& p, double t_min, double t_max, double d2_max,
   c.sx_prec = 1.0 / p.sigma_x;
   c.omega = 1.0 / p.sigma_t;
   const double inv_area = 1.0 / p.area;
-  c.a = p.mu0 * inv_area * c.tau_prec * kInvSqrt2Pi;         // model.hpp:329-331
-  c.c = p.xi0 * c.omega * c.sx_prec * c.sx_prec * kInv2Pi;   // model.hpp:333-336
-  c.half_s2 = 0.5 * c.sx_prec * c.sx_prec;                   // model.hpp:277
+  c.a = p.mu0 * inv_area * c.tau_prec * kInvSqrt2Pi;         // model.hpp:203-205
+  c.c = p.xi0 * c.omega * c.sx_prec * c.sx_prec * kInv2Pi;   // model.hpp:207-210
+  c.half_s2 = 0.5 * c.sx_prec * c.sx_prec;                   // model.hpp:151
   c.Kb = -0.5 * c.tau_prec * c.tau_prec * kLog2eT;
   c.Kq0 = -c.half_s2 * kLog2eT;
   c.Kw = -c.omega * kLog2eT;

@@ -68,7 +68,7 @@ std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g,
 int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
                int rows_per_item, std::vector<Item>& items, int window = 1);
 
-// Per-evaluation coefficients (types.hpp:105-109, model.hpp:328-336) and
+// Per-evaluation coefficients (types.hpp:105-109, model.hpp:202-210) and
 // the host-side argument bound that selects the checked exp.
 EvalCoef make_coef(const ParamsIn& p, double t_min, double t_max, double d2_max, double q_max);
 

@@ -9,15 +9,15 @@
 //                     tiles are staged in shared memory with bulk-async
 //                     copies (cp.async.bulk + mbarrier, double-buffered).
 //                     Five FP64 accumulators per row:
-//                       B  = sum_{t_j != t_i} b_ij          (model.hpp:250-266)
+//                       B  = sum_{t_j != t_i} b_ij          (model.hpp:124-140)
 //                       B2 = sum (t_i-t_j)^2 b_ij            (gradient, new)
-//                       T  = sum_{t_j < t_i} g_ij            (model.hpp:272-296)
+//                       T  = sum_{t_j < t_i} g_ij            (model.hpp:146-170)
 //                       Td = sum (t_i-t_j) g_ij              (gradient, new)
 //                       Tq = sum q_j d_ij^2 g_ij             (gradient, new)
 //                     with b_ij = exp(-(t_i-t_j)^2 / 2 tau^2) and
 //                     g_ij = q_j exp(-omega (t_i-t_j) - q_j d_ij^2 / 2 sigma_x^2).
 //   3. finish O(N)    combines partial slots in a fixed order, forms
-//                     ell_n = log(max(S_n, 1e-40)) - Lambda_n (model.hpp:301-349)
+//                     ell_n = log(max(S_n, 1e-40)) - Lambda_n (model.hpp:175-223)
 //                     and d ell_n / d theta, block-reduces to 6 doubles.
 //   4. reduce         fixed-order sum of the block partials.
 // No floating-point atomics anywhere: results are bitwise deterministic.
@@ -32,7 +32,7 @@
 //   B   every column after every row's ties: background only, no guards.
 //   M   the band around the rows' own times: per-pair guards
 //       t_j != t_i (as j outside [lb_i, ub_i)) and t_j < t_i (j < lb_i),
-//       exactly the reference's value guards (model.hpp:263, :278).
+//       exactly the reference's value guards (model.hpp:137, :152).
 //   BTx/Bx  BT/B tiles whose background is evaluated by the exact block
 //       expansion (kXP below) instead of per pair.
 //   skip tiles whose every term flushes to zero in this arithmetic.
@@ -397,7 +397,7 @@ constexpr float kEx2Shift = 24.0f;
 constexpr double kEx2Unscale = 5.9604644775390625e-08;  // 2^-24
 
 // Precision::single trigger of a BT/BTx/T tile (the reference's float path,
-// model.hpp:183-208 / :271-296, evaluated with MUFU ex2): FP32 distances in
+// model.hpp:57-82 / :271-296, evaluated with MUFU ex2): FP32 distances in
 // the centred frame, FP32 partial sums within the tile, then the FP64 row
 // factor exp(-omega (t_i - t_ref)) and an FP64 accumulator across tiles.
 template <int NR, bool kVarying, int kMode, bool kC = false>
@@ -946,11 +946,11 @@ __global__ void collapse_kernel(const double* __restrict__ partial, int slots, i
 }
 
 __device__ __forceinline__ double gaussian_cdf(double z) {
-  return 0.5 * erfc(-z * 0.7071067811865475244);  // model.hpp:157-160
+  return 0.5 * erfc(-z * 0.7071067811865475244);  // model.hpp:31-34
 }
 
 __device__ __forceinline__ double gaussian_pdf(double z) {
-  return kInvSqrt2Pi * exp(-0.5 * z * z);  // model.hpp:152-155
+  return kInvSqrt2Pi * exp(-0.5 * z * z);  // model.hpp:26-29
 }
 
 __global__ void __launch_bounds__(kFinishThreads) finish_kernel(
@@ -967,8 +967,8 @@ __global__ void __launch_bounds__(kFinishThreads) finish_kernel(
     const double T = tr_sums[li], Td = tr_sums[plane + li], Tq = tr_sums[2 * plane + li];
     const double ti = d.t[rows_base + li];
     const double S = c.a * B + c.c * T;
-    const double lg = log(fmax(S, kRateClip));  // == combine_lanes, model.hpp:311-326
-    // integral_term, model.hpp:301-306
+    const double lg = log(fmax(S, kRateClip));  // == combine_lanes, model.hpp:185-200
+    // integral_term, model.hpp:175-180
     const double r = c.t_end - ti;
     const double Phi_r = gaussian_cdf(r / c.tau_t);
     const double Phi_0 = gaussian_cdf(-ti / c.tau_t);
@@ -1019,6 +1019,78 @@ __global__ void __launch_bounds__(kFinishThreads) reduce_kernel(const double* __
     __syncthreads();
   }
   if (tid < 6) out6[tid] = s_red[tid][0];
+}
+
+// ---------------------------------------------------------------------------
+// location bounding box + finiteness (hk_set_locations), and the fixed-order
+// sum of per-device 6-vectors (multi-device contexts)
+
+constexpr int kBoxThreads = 256;
+constexpr int kBoxBlocks = 296;  // 2 per SM
+
+__global__ void __launch_bounds__(kBoxThreads)
+    bbox_partial_kernel(const double* __restrict__ x, const double* __restrict__ y, int n,
+                        double* part, int* bad) {
+  __shared__ double s[4][kBoxThreads];
+  __shared__ int sb[kBoxThreads];
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  double x0 = kInf, x1 = -kInf, y0 = kInf, y1 = -kInf;
+  int b = n;  // first non-finite index seen by this thread
+  for (int i = blockIdx.x * kBoxThreads + threadIdx.x; i < n; i += gridDim.x * kBoxThreads) {
+    const double xi = x[i], yi = y[i];
+    if (!isfinite(xi) || !isfinite(yi)) {
+      b = min(b, i);
+      continue;
+    }
+    x0 = fmin(x0, xi);
+    x1 = fmax(x1, xi);
+    y0 = fmin(y0, yi);
+    y1 = fmax(y1, yi);
+  }
+  s[0][threadIdx.x] = x0;
+  s[1][threadIdx.x] = x1;
+  s[2][threadIdx.x] = y0;
+  s[3][threadIdx.x] = y1;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int h = kBoxThreads / 2; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      s[0][threadIdx.x] = fmin(s[0][threadIdx.x], s[0][threadIdx.x + h]);
+      s[1][threadIdx.x] = fmax(s[1][threadIdx.x], s[1][threadIdx.x + h]);
+      s[2][threadIdx.x] = fmin(s[2][threadIdx.x], s[2][threadIdx.x + h]);
+      s[3][threadIdx.x] = fmax(s[3][threadIdx.x], s[3][threadIdx.x + h]);
+      sb[threadIdx.x] = min(sb[threadIdx.x], sb[threadIdx.x + h]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 4) part[blockIdx.x * 4 + threadIdx.x] = s[threadIdx.x][0];
+  if (threadIdx.x == 0) bad[blockIdx.x] = sb[0];
+}
+
+// out: {xmin, xmax, ymin, ymax, first non-finite index (n if none)} as doubles
+__global__ void bbox_final_kernel(const double* __restrict__ part, const int* __restrict__ bad,
+                                  int blocks, double* out) {
+  if (threadIdx.x != 0) return;
+  double v[4] = {part[0], part[1], part[2], part[3]};
+  int b = bad[0];
+  for (int k = 1; k < blocks; ++k) {
+    v[0] = fmin(v[0], part[4 * k + 0]);
+    v[1] = fmax(v[1], part[4 * k + 1]);
+    v[2] = fmin(v[2], part[4 * k + 2]);
+    v[3] = fmax(v[3], part[4 * k + 3]);
+    b = min(b, bad[k]);
+  }
+  for (int k = 0; k < 4; ++k) out[k] = v[k];
+  out[4] = static_cast<double>(b);
+}
+
+// total[k] = sum_d parts[d * 6 + k], d ascending (deterministic)
+__global__ void sum6_kernel(const double* __restrict__ parts, int n_dev, double* total) {
+  const int k = threadIdx.x;
+  if (k >= 6) return;
+  double a = 0.0;
+  for (int d = 0; d < n_dev; ++d) a += parts[d * 6 + k];
+  total[k] = a;
 }
 
 // ---------------------------------------------------------------------------
@@ -1157,6 +1229,20 @@ int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* bg_su
                                                    with_grad ? 1 : 0, ell_rows, grad_rows,
                                                    blockpart);
   return blocks;
+}
+
+int bbox_scratch_doubles() { return kBoxBlocks * 5; }
+
+void launch_bbox(const double* x, const double* y, int n, double* scratch, double* out5,
+                 cudaStream_t s) {
+  double* part = scratch;
+  int* bad = reinterpret_cast<int*>(scratch + 4 * kBoxBlocks);
+  bbox_partial_kernel<<<kBoxBlocks, kBoxThreads, 0, s>>>(x, y, n, part, bad);
+  bbox_final_kernel<<<1, 32, 0, s>>>(part, bad, kBoxBlocks, out5);
+}
+
+void launch_sum6(const double* parts, int n_dev, double* total, cudaStream_t s) {
+  sum6_kernel<<<1, 32, 0, s>>>(parts, n_dev, total);
 }
 
 void launch_reduce(const double* blockpart, int n_blocks, double* out6, cudaStream_t s) {

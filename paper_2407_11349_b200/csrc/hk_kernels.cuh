@@ -17,17 +17,25 @@ namespace hk {
 struct Item {
   int rb, re, tb, te, slot, pos;
 };
-constexpr int kMaxItemTiles = 1024;  // te - tb (the pair kernel classifies them in shared memory)
+constexpr int kMaxItemTiles = 2048;  // te - tb (the pair kernel classifies them in shared memory)
+// Work items per launch the planner aims for (~72 waves of 148 SMs x 3
+// CTAs): measured at N=1e6 (tools/item_sweep.sh, profiles/r02_item_sweep.txt)
+// the pair kernel keeps speeding up with more, smaller items up to here
+// (3552 items: 543.5 ms, 7104: 522.9, 14208: 510.1, 31264: 503.9).
+constexpr int kItemTarget = 148 * 3 * 72;
+// Column chunks per row block at most: the partial-sum buffer holds
+// slots x 40 B per row.
+constexpr int kMaxSlots = 64;
 
 // Per-evaluation coefficients, all derived on the host in double exactly
 // once (HawkesParams accessors, types.hpp:105-109; coefficients,
-// model.hpp:328-336).
+// model.hpp:202-210).
 struct EvalCoef {
   double mu0, tau_t, xi0, sigma_x, sigma_t;
   double tau_prec, sx_prec, omega;
   double a;       // background_coefficient<double>
   double c;       // trigger_coefficient<double>
-  double half_s2; // 0.5 * sx_prec * sx_prec (model.hpp:277)
+  double half_s2; // 0.5 * sx_prec * sx_prec (model.hpp:151)
   double Kb;      // -0.5 tau_prec^2 * 16/ln2   (background exponent per td^2)
   double Kq0;     // -half_s2 * 16/ln2           (trigger exponent per d^2, q = 1)
   double Kw;      // -omega * 16/ln2             (trigger exponent per td)
@@ -48,7 +56,7 @@ struct DeviceCatalog {
   const double* x;   // [npad], padded with 0
   const double* y;   // [npad]
   const double* q;   // density, [npad], padded with 1
-  const int* lb;     // [n] count_before(t_i) (model.hpp:241-243)
+  const int* lb;     // [n] count_before(t_i) (model.hpp:115-117)
   const int* ub;     // [n] upper_bound(t_i)
   double* K;         // prep: per-source trigger exponent coefficient  [npad]
   double* thr;       // prep: d^2 beyond which the spatial factor flushes [npad]
@@ -107,6 +115,14 @@ int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* bg_su
                   const double* tr_sums, int rows_base, int rows_total, bool with_grad,
                   double* ell_rows, double* grad_rows, double* blockpart, cudaStream_t s);
 void launch_reduce(const double* blockpart, int n_blocks, double* out6, cudaStream_t s);
+// Bounding box and finiteness of n locations: out5 = {xmin, xmax, ymin, ymax,
+// index of the first non-finite location or n}, on the device; scratch holds
+// bbox_scratch_doubles() doubles.
+int bbox_scratch_doubles();
+void launch_bbox(const double* x, const double* y, int n, double* scratch, double* out5,
+                 cudaStream_t s);
+// total[k] = sum over d < n_dev of parts[6 d + k], in ascending d.
+void launch_sum6(const double* parts, int n_dev, double* total, cudaStream_t s);
 double measure_fp64_peak(int device, double* ms);
 
 }  // namespace hk

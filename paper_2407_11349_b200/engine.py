@@ -11,7 +11,7 @@ Names, argument meaning and error behaviour follow the reference:
   HawkesParams + validate      types.hpp:83-110  HawkesParams
   Partition::make              engine.hpp:22-43  Partition.make / make_partition
   log_likelihood               engine.hpp:101-110 log_likelihood
-  event_contribution           model.hpp:351-356 event_contribution
+  event_contribution           model.hpp:225-230 event_contribution
   LikelihoodWorkspace<double>  engine.hpp:117-229 LikelihoodWorkspace
   benchmark_catalog            engine.hpp:251-259 benchmark_catalog
   (new)                                          log_likelihood_and_gradient
@@ -167,11 +167,17 @@ class Evaluator:
     """One engine context: the catalog resident on `n_gpus` devices (or one
     rank's row shard on `device`)."""
 
-    def __init__(self, catalog: Catalog, n_gpus: int = 1, shard=None, device: int = 0):
+    def __init__(self, catalog: Catalog, n_gpus: int = 1, shard=None, device: int = 0, devices=None,
+                 plan_for: "Variant | int" = 0):
         self.catalog = catalog
         h = C.c_void_p()
         t, x, y, d = catalog.arrays()
-        if shard is None:
+        if devices is not None:
+            # one cost-balanced shard per entry; distinct devices exchange the
+            # 6-vectors and locations over NCCL, a repeated device by peer copies
+            dv = np.ascontiguousarray(devices, dtype=np.int32)
+            check(lib.hk_create_devices(t, x, y, d, len(t), dv, len(dv), int(plan_for), C.byref(h)))
+        elif shard is None:
             check(lib.hk_create(t, x, y, d, len(t), n_gpus, C.byref(h)))
         else:
             b, e = shard
@@ -208,6 +214,21 @@ class Evaluator:
                           g.ctypes.data_as(C.c_void_p) if grad else None))
         return (ll.value, g) if grad else ll.value
 
+    def eval_detail(self, params: HawkesParams, grad: bool = True):
+        """hk_eval plus the per-row ell_n (and d ell_n / d theta) of the same
+        production launches, for the context's rows [begin, end)."""
+        b, e, _ = self.rows()
+        p = params.to_c()
+        ll = C.c_double()
+        g = np.zeros(5)
+        ell = np.zeros(e - b)
+        gr = np.zeros((e - b, 5)) if grad else None
+        check(lib.hk_eval_detail(self._h, C.byref(p), C.byref(ll),
+                                 g.ctypes.data_as(C.c_void_p) if grad else None,
+                                 ell.ctypes.data_as(C.c_void_p),
+                                 gr.ctypes.data_as(C.c_void_p) if grad else None))
+        return (ll.value, g, ell, gr) if grad else (ll.value, ell)
+
     def eval_single(self, params: HawkesParams) -> float:
         """Precision.single: FP32 trigger arithmetic, log-likelihood only."""
         p = params.to_c()
@@ -225,6 +246,13 @@ class Evaluator:
         check(lib.hk_ws_eval(self._h, C.byref(p), int(force), C.byref(ll),
                              g.ctypes.data_as(C.c_void_p) if grad else None))
         return (ll.value, g) if grad else ll.value
+
+    def ws_eval_single(self, params: HawkesParams, force: bool = False) -> float:
+        """Single-precision workspace evaluation (hk_ws_eval_single), LL only."""
+        p = params.to_c()
+        ll = C.c_double()
+        check(lib.hk_ws_eval_single(self._h, C.byref(p), int(force), C.byref(ll)))
+        return ll.value
 
     def ws_stats(self):
         h, m = C.c_long(), C.c_long()
@@ -264,6 +292,13 @@ class Evaluator:
         check(lib.hk_profile(self._h, C.byref(ms), C.byref(npair), C.byref(ntot)))
         return ms.value, npair.value, ntot.value
 
+    def profile_kinds(self):
+        """(ms[3], launches[3]) of the pair launches by kind: both halves,
+        background only, trigger only."""
+        ms, n = np.zeros(3), np.zeros(3, dtype=np.int64)
+        check(lib.hk_profile_kinds(self._h, ms, n))
+        return ms, n
+
     def reset_profile(self) -> None:
         check(lib.hk_reset_profile(self._h))
 
@@ -301,7 +336,7 @@ def log_likelihood_and_gradient(catalog: Catalog, p: HawkesParams, part: Partiti
 
 
 def event_contribution(p: HawkesParams, catalog: Catalog, n: int) -> float:
-    """model.hpp:351-356."""
+    """model.hpp:225-230."""
     if n < 0 or n >= catalog.size():
         raise IndexError("event_contribution: index out of range")
     p.validate()
@@ -313,18 +348,30 @@ class LikelihoodWorkspace:
     the per-row background [B, B2] and trigger [T, Td, Tq] sums cached on the
     device: a mu0/xi0 proposal recombines cached sums in O(N), tau_t refreshes
     only the background, sigma_x/sigma_t (or set_locations) only the trigger.
-    Results are bitwise identical to a fresh evaluation at every setting."""
+    Results are bitwise identical to a fresh evaluation at every setting.
+    precision=Precision.single is LikelihoodWorkspace<float>: the same
+    caches over the FP32 trigger arithmetic of Precision.single (LL only)."""
 
-    def __init__(self, catalog: Catalog, variant: Variant, workers: int = 1):
+    def __init__(self, catalog: Catalog, variant: Variant, workers: int = 1,
+                 precision: Precision = Precision.dbl):
         self._catalog = catalog
         self._variant = Variant(variant)
+        self._single = precision == Precision.single
         self._ev = Evaluator(catalog)
 
+    def _eval(self, p: HawkesParams, grad: bool, force: bool):
+        p = replace(p, variant=self._variant)
+        if self._single:
+            if grad:
+                raise ValueError("LikelihoodWorkspace<float>: the gradient is double precision only")
+            return self._ev.ws_eval_single(p, force=force)
+        return self._ev.ws_eval(p, grad=grad, force=force)
+
     def evaluate_full(self, p: HawkesParams, grad: bool = False):
-        return self._ev.ws_eval(replace(p, variant=self._variant), grad=grad, force=True)
+        return self._eval(p, grad, True)
 
     def evaluate_proposal(self, p: HawkesParams, grad: bool = False):
-        return self._ev.ws_eval(replace(p, variant=self._variant), grad=grad)
+        return self._eval(p, grad, False)
 
     def commit_proposal(self) -> None:
         """The device cache keeps the current and the proposal state (two

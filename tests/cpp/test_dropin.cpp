@@ -6,6 +6,7 @@
 // (acceptance.cpp convention).  Built where /root/reference exists
 // (oracle/Makefile `dropin`), run on a GPU box (tests/test_dropin.py).
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <random>
@@ -145,7 +146,7 @@ void contributions_and_errors() {
   } catch (const std::out_of_range&) {
     ok3 = true;
   }
-  report("exception types and messages (types.hpp:92-103, engine.hpp:104-105, model.hpp:352)",
+  report("exception types and messages (types.hpp:92-103, engine.hpp:104-105, model.hpp:226)",
          ok && ok2 && ok3, "invalid_argument / out_of_range");
 }
 
@@ -314,9 +315,42 @@ void sampler_cut_unchanged() {
   report("mcmc.hpp cut-posterior sampler (coarse catalog) unchanged on the B200 workspace", same, d);
 }
 
+// The free functions keep the last catalog's engine (include/hawkes_b200/
+// engine.hpp, detail::with_cached_engine): results must follow the catalog's
+// CONTENT (a one-event change is a different catalog) and a repeated call
+// must skip the context build.
+void engine_cache_keyed_by_content() {
+  std::mt19937_64 rng(77);
+  const Catalog a = random_catalog(rng, 60000);
+  std::vector<Event> ev = a.events();
+  ev[123].lon += 1e-9;  // same size, same address pattern, different content
+  const Catalog b(std::move(ev));
+  HawkesParams p = random_params(rng);
+  p.variant = Variant::varying;
+  const Partition part = make_partition(a.size(), 1);
+  auto timed = [&](const Catalog& c) {
+    const auto t0 = std::chrono::steady_clock::now();
+    const double v = b200::log_likelihood(c, p, part, Precision::dbl);
+    return std::make_pair(v, std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+  };
+  const auto a1 = timed(a);
+  const auto b1 = timed(b);  // rebuild
+  const auto b2 = timed(b);  // cached
+  const auto a2 = timed(a);  // rebuild
+  const double fa = b200::Engine(a).log_likelihood(p, p.variant);
+  const double fb = b200::Engine(b).log_likelihood(p, p.variant);
+  const bool ok = a1.first == fa && a2.first == fa && b1.first == fb && b2.first == fb && fa != fb &&
+                  b2.second < 0.5 * a2.second;
+  char d[160];
+  std::snprintf(d, sizeof d, "rebuild %.1f ms, cached call %.1f ms, A != B: %d", a2.second * 1e3,
+                b2.second * 1e3, fa != fb);
+  report("free functions reuse the catalog's engine, keyed by content", ok, d);
+}
+
 }  // namespace
 
 int main() {
+  engine_cache_keyed_by_content();
   engine_agrees_with_naive();
   criterion_1_subset();
   contributions_and_errors();

@@ -6,9 +6,15 @@
 //      (CPU) give posterior means within 4 Monte Carlo standard errors on a
 //      simulated catalog (acceptance.cpp:244-296 convention);
 //   3. the HMC chain persists through the reference's chain CSV and sidecar
-//      writers (io.hpp:129-156) and reads back exactly (read_chain_csv).
+//      writers (io.hpp:129-156) and reads back exactly (read_chain_csv);
+//   4. with real (square) regions every loglik_trace entry is the
+//      log-likelihood of that draw at that iteration's locations (the
+//      reference's location stream, replayed here), including after rejected
+//      transitions that follow an X refresh.
 // PASS/FAIL lines; exit status = number of failures.
+#include <algorithm>
 #include <cmath>
+#include <random>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -152,9 +158,82 @@ void posterior_agreement() {
   report("HMC (GPU gradient) and reference MH agree on the posterior", worst <= 4.0, detail + b);
 }
 
+// Square counties over the simulation window; each event tagged with its
+// containing square (clamped to the grid) and that county's density.
+PointSetup square_regions(const Catalog& catalog, int grid) {
+  RegionTable regions;
+  std::mt19937_64 drng(3);
+  std::uniform_real_distribution<double> ulog(0.0, std::log(50.0));
+  const double lo = -1.0, cell = 2.0 / grid;
+  for (int gy = 0; gy < grid; ++gy)
+    for (int gx = 0; gx < grid; ++gx) {
+      const double x0 = lo + gx * cell, y0 = lo + gy * cell;
+      Region r;
+      r.id = "s" + std::to_string(gy * grid + gx);
+      r.polygons.push_back(
+          PolygonShape{{{x0, y0}, {x0 + cell, y0}, {x0 + cell, y0 + cell}, {x0, y0 + cell}}, {}});
+      r.density = std::exp(ulog(drng));
+      r.representative_latitude = y0 + 0.5 * cell;
+      regions.add(std::move(r));
+    }
+  std::vector<Event> tagged = catalog.events();
+  for (Event& e : tagged) {
+    const int gx = std::clamp(static_cast<int>(std::floor((e.lon - lo) / cell)), 0, grid - 1);
+    const int gy = std::clamp(static_cast<int>(std::floor((e.lat - lo) / cell)), 0, grid - 1);
+    e.region_id = "s" + std::to_string(gy * grid + gx);
+    e.density = regions.at(e.region_id).density;
+  }
+  return {Catalog(std::move(tagged)), std::move(regions)};
+}
+
+void loglik_trace_matches_locations() {
+  const PointSetup setup = square_regions(simulated(), 4);
+  b200::HmcConfig cfg;
+  cfg.chain = base_config(setup.tagged);
+  cfg.chain.initial.variant = Variant::varying;
+  cfg.chain.iterations = 60;
+  cfg.chain.burn_in = 10;
+  cfg.chain.refresh_period = 1;
+  cfg.leapfrog_steps = 4;
+  cfg.step_size = 0.3;  // large: many rejections right after an X refresh
+  cfg.adapt = false;
+  const ChainOutput out = b200::run_cut_posterior_hmc(cfg, setup.tagged, setup.regions);
+  // replay the location stream: the constructor's draw, then one per refresh
+  std::mt19937_64 rng(cfg.chain.seed);
+  resample_locations(setup.tagged, setup.regions, rng);
+  b200::Engine check(setup.tagged);
+  double worst = 0.0;
+  std::size_t rejected = 0, compared = 0;
+  bool ok = out.loglik_trace.size() == out.draws.size();
+  for (std::size_t iter = 0; ok && iter < cfg.chain.iterations; ++iter) {
+    if (iter % cfg.chain.refresh_period == 0) {
+      auto [lon, lat] = resample_locations(setup.tagged, setup.regions, rng);
+      check.set_locations(lon, lat);
+    }
+    if (iter < cfg.chain.burn_in) continue;
+    const std::size_t i = iter - cfg.chain.burn_in;
+    HawkesParams p = cfg.chain.initial;
+    p.mu0 = out.draws[i][0];
+    p.tau_t = out.draws[i][1];
+    p.xi0 = out.draws[i][2];
+    p.sigma_x = out.draws[i][3];
+    p.sigma_t = out.draws[i][4];
+    std::array<double, 5> g{};
+    const double want = check.log_likelihood_and_gradient(p, p.variant, g);
+    worst = std::max(worst, std::abs(out.loglik_trace[i] - want) / std::max(1.0, std::abs(want)));
+    if (i > 0 && out.draws[i] == out.draws[i - 1]) ++rejected;
+    ++compared;
+  }
+  ok = ok && worst <= 1e-12 && rejected > 0;
+  report("cut-posterior HMC: loglik_trace[i] == LL(draw i, X of iteration i)", ok,
+         std::to_string(compared) + " draws, " + std::to_string(rejected) +
+             " rejected after a refresh, worst rel diff " + std::to_string(worst));
+}
+
 }  // namespace
 
 int main() {
+  loglik_trace_matches_locations();
   point_regions_collapse();
   posterior_agreement();
   std::printf("%d failure(s)\n", failures);

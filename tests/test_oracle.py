@@ -152,11 +152,16 @@ def test_oracle_kats(oracle):
 
 
 @pytest.mark.parametrize("case", golden("acceptance1.json")[:12], ids=lambda c: f"n{c['n']}v{c['variant']}")
-def test_oracle_lanes_match_reference_bitwise(oracle, case):
+def test_oracle_lanes_match_reference(oracle, case):
+    """The C restatement of the lane evaluator against the reference's own
+    values: equal to within 4 ulp (45 of the 48 (catalog, G) values are
+    bitwise equal; the rest differ in the last bit because the reference is
+    built with -march=native and GCC contracts some of its products into
+    FMAs differently than the -O2 scalar restatement)."""
     cat = golden_catalog(case)
     assert digest(cat) == case["sha256"]
     for g, v in case["ll"].items():
-        assert oracle.log_likelihood(cat, case["params"], case["variant"], int(g)) == pytest.approx(v, rel=1e-13)
+        assert oracle.log_likelihood(cat, case["params"], case["variant"], int(g)) == pytest.approx(v, rel=1e-15)
     assert oracle.naive_log_likelihood(cat, case["params"], case["variant"]) == pytest.approx(case["naive"], rel=1e-14)
 
 
