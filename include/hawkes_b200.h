@@ -165,6 +165,39 @@ const double* hk_result_device(hk_ctx* ctx);
 /* cudaStream_t (as void*) the context launches on, for device index `dev`. */
 void* hk_stream(hk_ctx* ctx, int dev);
 
+/* ---- GPU location sampler (the cut posterior's X refresh) ----------------
+ *
+ * resample_locations (mcmc.hpp:80-97) -> sample_point_in_region
+ * (geo.hpp:138-161) as one GPU thread per event: area-weighted polygon part,
+ * bounding-box rejection against the even-odd point-in-polygon test (outer
+ * ring minus holes), 10000 attempts; point regions return their point.  The
+ * random stream is Philox4x32-10 keyed by `seed` with counter (event,
+ * `counter`), NOT the reference's mt19937_64: draws are reproducible for a
+ * fixed (seed, counter) and match the reference in distribution.
+ *
+ * Region table, flattened (a RegionTable, geo.hpp:85-113):
+ *   is_point[R], point_xy[2R]          Region::is_point / point
+ *   region_parts[R+1]                  region r owns parts [region_parts[r], region_parts[r+1])
+ *   part_rings[P+1]                    part p owns rings [part_rings[p], part_rings[p+1]);
+ *                                      the first is the outer ring, the rest holes
+ *   ring_verts[Rings+1], verts[2V]     ring g's vertices (lon, lat) pairs
+ *   region_ids[R] (nullable)           Region::id, for error messages
+ *   event_region[N]                    each catalog event's region index
+ * Failures (zero-area region, exhausted attempts) return HK_RUNTIME_ERROR
+ * with the reference's runtime_error message and the event index. */
+typedef struct hk_regions hk_regions;
+int hk_regions_create(size_t n_regions, const int* is_point, const double* point_xy,
+                      const size_t* region_parts, const size_t* part_rings, const size_t* ring_verts,
+                      const double* verts, const char* const* region_ids, size_t n_events,
+                      const int* event_region, int device, hk_regions** out);
+void hk_regions_destroy(hk_regions* regions);
+/* One draw for every event into host arrays lon[N], lat[N]. */
+int hk_regions_sample(hk_regions* regions, uint64_t seed, uint64_t counter, double* lon, double* lat);
+/* One draw for every event straight into the context's device locations
+ * (then the hk_set_locations check and broadcast); the region table must
+ * live on the context's first device. */
+int hk_resample_locations(hk_ctx* ctx, hk_regions* regions, uint64_t seed, uint64_t counter);
+
 /* Per-row contributions ell_n for rows [b, e) (slice_log_likelihood on
  * single rows, engine.hpp:65-83).  ell_rows has e-b entries; grad_rows, if
  * non-NULL, has 5*(e-b) entries (row-major, 5 per row).  Rows must lie in

@@ -116,6 +116,11 @@ class Engine {
     detail::check(hk_set_locations(ctx_.get(), lon.data(), lat.data()));
   }
 
+  // GPU X refresh straight into the device locations (hawkes_b200/regions.hpp).
+  void resample_locations(hk_regions* regions, std::uint64_t seed, std::uint64_t counter) {
+    detail::check(hk_resample_locations(ctx_.get(), regions, seed, counter));
+  }
+
   // Device-cached workspace evaluation (hk_ws_eval).
   double workspace_eval(const HawkesParams& p, Variant v, bool force, double* grad5 = nullptr) {
     const hk_params c = detail::to_c(p, v);

@@ -16,12 +16,16 @@
 //   * step size adapted by dual averaging during burn-in (Hoffman & Gelman
 //     2014, section 3.2), frozen afterwards so the post-burn-in kernel is fixed
 //     (mcmc.hpp:99-111 convention);
-//   * the X refresh is the reference's own resample_locations
+//   * the X refresh is by default the reference's own resample_locations
 //     (mcmc.hpp:80-97) on its own RNG stream (location_rng_, seeded like
 //     mcmc.hpp:126), so the sequence of location draws is the reference's.
 //     Because X does not depend on Theta (cut posterior), the next draw is
 //     computed on a host thread while the GPU runs the current iteration's
 //     leapfrog steps (overlap the resample).
+//     HmcConfig::gpu_resample = true draws X on the GPU instead
+//     (hawkes_b200/regions.hpp: the same algorithm, one thread per event,
+//     Philox-keyed by (seed, refresh index)) straight into the engine's
+//     device locations: no host resample, no location upload.
 //
 // Output is the reference's ChainOutput (mcmc.hpp:63-76), so its chain CSV /
 // sidecar writers and diagnostics apply unchanged.  The per-iteration time
@@ -35,6 +39,7 @@
 #include <cmath>
 #include <cstdint>
 #include <future>
+#include <memory>
 #include <random>
 #include <stdexcept>
 #include <utility>
@@ -43,6 +48,7 @@
 #include "hawkes/geo.hpp"
 #include "hawkes/mcmc.hpp"
 #include "hawkes_b200/engine.hpp"
+#include "hawkes_b200/regions.hpp"
 
 namespace hawkes::b200 {
 
@@ -54,6 +60,7 @@ struct HmcConfig {
   bool adapt = true;
   std::array<double, kParamCount> scales{1, 1, 1, 1, 1};  // diagonal metric (inverse mass sqrt)
   int n_gpus = 1;
+  bool gpu_resample = false;      // X refresh on the GPU (Philox stream) instead of the reference's
 };
 
 struct HmcTiming {
@@ -83,8 +90,11 @@ class HmcSampler {
     eps_ = cfg_.step_size;
     log_eps_bar_ = 0.0;
     mu_ = std::log(10.0 * eps_);
-    if (regions_ != nullptr) {
-      auto [lon, lat] = resample_locations(*catalog_, *regions_, location_rng_);
+    if (regions_ != nullptr && cfg_.gpu_resample) {
+      gpu_regions_ = std::make_unique<GpuRegions>(catalog, *regions_);
+      engine_.resample_locations(gpu_regions_->get(), cfg_.chain.seed, refresh_count_++);
+    } else if (regions_ != nullptr) {
+      auto [lon, lat] = hawkes::resample_locations(*catalog_, *regions_, location_rng_);
       engine_.set_locations(lon, lat);
     }
     value_ = log_density(z_, grad_);
@@ -95,22 +105,29 @@ class HmcSampler {
     const auto start = std::chrono::steady_clock::now();
     ChainOutput out;
     std::future<std::pair<std::vector<double>, std::vector<double>>> next;
+    const bool host_resample = regions_ != nullptr && !cfg_.gpu_resample;
     auto prefetch = [&] {
-      if (regions_ != nullptr)
+      if (host_resample)
         next = std::async(std::launch::async,
-                          [this] { return resample_locations(*catalog_, *regions_, location_rng_); });
+                          [this] { return hawkes::resample_locations(*catalog_, *regions_, location_rng_); });
     };
     prefetch();
     for (std::size_t iter = 0; iter < cfg_.chain.iterations; ++iter) {
       if (regions_ != nullptr && iter % cfg_.chain.refresh_period == 0) {
-        auto t0 = clock::now();
-        auto [lon, lat] = next.get();  // X draw for this iteration (reference stream order)
-        auto t1 = clock::now();
-        prefetch();                    // the next draw overlaps this iteration's GPU work
-        engine_.set_locations(lon, lat);
-        auto t2 = clock::now();
-        timing_.resample_wait += seconds(t0, t1);
-        timing_.set_locations += seconds(t1, t2);
+        if (host_resample) {
+          auto t0 = clock::now();
+          auto [lon, lat] = next.get();  // X draw for this iteration (reference stream order)
+          auto t1 = clock::now();
+          prefetch();                    // the next draw overlaps this iteration's GPU work
+          engine_.set_locations(lon, lat);
+          auto t2 = clock::now();
+          timing_.resample_wait += seconds(t0, t1);
+          timing_.set_locations += seconds(t1, t2);
+        } else {
+          auto t0 = clock::now();
+          engine_.resample_locations(gpu_regions_->get(), cfg_.chain.seed, refresh_count_++);
+          timing_.resample_wait += seconds(t0, clock::now());
+        }
         value_ = log_density(z_, grad_);  // the target changed with X
         loglik_ = last_ll_;  // a rejected transition keeps these locations' LL
       }
@@ -239,6 +256,8 @@ class HmcSampler {
   Engine engine_;
   std::mt19937_64 location_rng_;
   std::mt19937_64 param_rng_;
+  std::unique_ptr<GpuRegions> gpu_regions_;  // gpu_resample only
+  std::uint64_t refresh_count_ = 0;
   Vec z_{}, grad_{};
   double value_ = 0.0, loglik_ = 0.0, last_ll_ = 0.0;
   double eps_ = 0.02, mu_ = 0.0, h_bar_ = 0.0, log_eps_bar_ = 0.0;

@@ -5,11 +5,12 @@ every MCMC step of the cut-posterior sampler) as hand-written sm_100a CUDA
 behind a C ABI (include/hawkes_b200.h).  This package is the thin Python
 mirror of the reference's interface; see DESIGN.md.
 """
-from .engine import (Catalog, Evaluator, HawkesParams, LikelihoodWorkspace, Partition, Precision,
+from .engine import (Catalog, Evaluator, HawkesParams, LikelihoodWorkspace, Partition, Precision, Region, Regions,
                      Variant, benchmark_catalog, event_contribution, log_likelihood,
                      log_likelihood_and_gradient, make_partition, plan_shards)
 
 __all__ = [
+    "Region", "Regions",
     "Catalog", "Evaluator", "HawkesParams", "LikelihoodWorkspace", "Partition", "Precision",
     "Variant", "benchmark_catalog", "event_contribution", "log_likelihood",
     "log_likelihood_and_gradient", "make_partition", "plan_shards",

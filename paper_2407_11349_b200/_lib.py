@@ -59,6 +59,13 @@ SIGNATURES = [
     ("hk_eval_async", C.c_int, [_ctx, _pp, C.c_int]),
     ("hk_result_device", C.c_void_p, [_ctx]),
     ("hk_stream", C.c_void_p, [_ctx, C.c_int]),
+    ("hk_regions_create", C.c_int, [_sz, np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS"), _dp,
+                                   _szp, _szp, _szp, _dp, C.c_void_p, _sz,
+                                   np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS"), C.c_int,
+                                   C.POINTER(C.c_void_p)]),
+    ("hk_regions_destroy", None, [C.c_void_p]),
+    ("hk_regions_sample", C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, _dp, _dp]),
+    ("hk_resample_locations", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_uint64]),
     ("hk_eval_rows", C.c_int, [_ctx, _pp, _sz, _sz, _dp, C.c_void_p]),
     ("hk_set_option", C.c_int, [_ctx, C.c_int, C.c_int]),
     ("hk_rows", C.c_int, [_ctx, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int)]),

@@ -33,6 +33,7 @@
 #include "hk_device.cuh"
 #include "hk_host.hpp"
 #include "hk_kernels.cuh"
+#include "hk_regions.hpp"
 
 namespace {
 
@@ -818,6 +819,121 @@ int hk_set_locations_device(hk_ctx* ctx, const double* lon_device, const double*
     ck(cudaMemcpyAsync(s.y, lat_device, ctx->n * sizeof(double), cudaMemcpyDeviceToDevice, s.stream),
        "set_locations_device");
     ctx->publish_locations();
+  });
+}
+
+// ---- GPU location sampler (hk_regions.cu) ------------------------------------
+
+}  // extern "C"
+
+struct hk_regions {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  hk::RegionsDevice d;
+  std::vector<std::string> ids;
+  unsigned long long* h_fail = nullptr;  // pinned
+  double *tmp_x = nullptr, *tmp_y = nullptr;  // hk_regions_sample's device outputs
+  ~hk_regions() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    hk::free_regions(d);
+    if (h_fail) cudaFreeHost(h_fail);
+    if (tmp_x) cudaFree(tmp_x);
+    if (tmp_y) cudaFree(tmp_y);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  std::string id(int r) const {
+    return r < static_cast<int>(ids.size()) ? ids[r] : std::to_string(r);
+  }
+
+  // The reference's messages (mcmc.hpp:87-95, geo.hpp:146-147, :158-159).
+  void throw_failure(unsigned long long word, const std::vector<int>& event_region) const {
+    const unsigned long long e = word >> 2;
+    const int r = event_region[e];
+    const std::string what = (word & 3) == hk::kFailZeroArea
+                                 ? "sample_point_in_region: region " + id(r) + " has zero area"
+                                 : "sample_point_in_region: rejection budget exhausted for region " + id(r);
+    throw std::runtime_error("resample_locations: event " + std::to_string(e) + ": " + what);
+  }
+  std::vector<int> event_region;
+};
+
+extern "C" {
+
+int hk_regions_create(size_t n_regions, const int* is_point, const double* point_xy,
+                      const size_t* region_parts, const size_t* part_rings, const size_t* ring_verts,
+                      const double* verts, const char* const* region_ids, size_t n_events,
+                      const int* event_region, int device, hk_regions** out) {
+  return guarded([&] {
+    if (!out || !is_point || !point_xy || !region_parts || !event_region)
+      throw std::invalid_argument("hk_regions_create: null argument");
+    if (region_parts[n_regions] > 0 && (!part_rings || !ring_verts || !verts))
+      throw std::invalid_argument("hk_regions_create: null polygon arrays");
+    if (n_events >= (std::size_t{1} << 31) - 1024)
+      throw std::invalid_argument("hk_regions_create: more than 2^31 events is not supported");
+    *out = nullptr;
+    auto reg = std::make_unique<hk_regions>();
+    const hk::RegionsHost h = hk::build_regions(n_regions, is_point, point_xy, region_parts, part_rings,
+                                                ring_verts, verts, n_events, event_region);
+    reg->device = device;
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&reg->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    reg->d = hk::upload_regions(h, reg->stream);
+    ck(cudaStreamSynchronize(reg->stream), "hk_regions_create");
+    ck(cudaMallocHost(&reg->h_fail, sizeof(unsigned long long)), "cudaMallocHost");
+    if (region_ids)
+      for (std::size_t r = 0; r < n_regions; ++r) reg->ids.emplace_back(region_ids[r] ? region_ids[r] : "");
+    reg->event_region = h.event_region;
+    *out = reg.release();
+  });
+}
+
+void hk_regions_destroy(hk_regions* regions) { delete regions; }
+
+int hk_regions_sample(hk_regions* regions, uint64_t seed, uint64_t counter, double* lon, double* lat) {
+  return guarded([&] {
+    if (!regions || !lon || !lat) throw std::invalid_argument("hk_regions_sample: null argument");
+    hk_regions& R = *regions;
+    ck(cudaSetDevice(R.device), "cudaSetDevice");
+    const std::size_t n = static_cast<std::size_t>(R.d.n_events);
+    if (!R.tmp_x) {
+      R.tmp_x = dmalloc<double>(n);
+      R.tmp_y = dmalloc<double>(n);
+    }
+    hk::launch_sample(R.d, seed, counter, R.tmp_x, R.tmp_y, R.stream);
+    ck(cudaGetLastError(), "sample kernel");
+    ck(cudaMemcpyAsync(R.h_fail, R.d.fail, sizeof(unsigned long long), cudaMemcpyDeviceToHost, R.stream),
+       "fail copy");
+    ck(cudaMemcpyAsync(lon, R.tmp_x, n * sizeof(double), cudaMemcpyDeviceToHost, R.stream), "copy");
+    ck(cudaMemcpyAsync(lat, R.tmp_y, n * sizeof(double), cudaMemcpyDeviceToHost, R.stream), "copy");
+    ck(cudaStreamSynchronize(R.stream), "hk_regions_sample");
+    if (*R.h_fail != ~0ull) R.throw_failure(*R.h_fail, R.event_region);
+  });
+}
+
+int hk_resample_locations(hk_ctx* ctx, hk_regions* regions, uint64_t seed, uint64_t counter) {
+  return guarded([&] {
+    if (!ctx || !regions) throw std::invalid_argument("hk_resample_locations: null argument");
+    hk_regions& R = *regions;
+    if (R.d.n_events != ctx->n)
+      throw std::invalid_argument("hk_resample_locations: region table is for " +
+                                  std::to_string(R.d.n_events) + " events, catalog has " +
+                                  std::to_string(ctx->n));
+    auto& s0 = ctx->devs[0];
+    if (R.device != s0.dev)
+      throw std::invalid_argument("hk_resample_locations: region table and context on different devices");
+    ck(cudaSetDevice(s0.dev), "cudaSetDevice");
+    hk::launch_sample(R.d, seed, counter, s0.x, s0.y, s0.stream);
+    ck(cudaGetLastError(), "sample kernel");
+    ck(cudaMemcpyAsync(R.h_fail, R.d.fail, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s0.stream),
+       "fail copy");
+    ctx->prof_total += 1;
+    ctx->publish_locations();  // box check on device 0, broadcast, trigger caches dropped
+    if (*R.h_fail != ~0ull) {
+      ctx->locations_valid = false;
+      R.throw_failure(*R.h_fail, R.event_region);
+    }
   });
 }
 

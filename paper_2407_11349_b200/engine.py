@@ -203,6 +203,11 @@ class Evaluator:
             raise ValueError("set_locations: length mismatch")
         check(lib.hk_set_locations(self._h, lon, lat))
 
+    def resample_locations(self, regions: "Regions", seed: int, counter: int = 0) -> None:
+        """GPU X refresh: one draw per event from its region straight into
+        this context's device locations (hk_resample_locations)."""
+        check(lib.hk_resample_locations(self._h, regions.handle, seed, counter))
+
     def set_locations_device(self, lon_ptr: int, lat_ptr: int) -> None:
         check(lib.hk_set_locations_device(self._h, C.c_void_p(lon_ptr), C.c_void_p(lat_ptr)))
 
@@ -341,6 +346,61 @@ def event_contribution(p: HawkesParams, catalog: Catalog, n: int) -> float:
         raise IndexError("event_contribution: index out of range")
     p.validate()
     return float(_evaluator_for(catalog).eval_rows(p, n, n + 1)[0])
+
+
+@dataclass
+class Region:
+    """A coarse region (geo.hpp:85-113): an exact point, or polygons, each a
+    list of rings [outer, hole, hole, ...], a ring an (m, 2) array of
+    (lon, lat) vertices."""
+    id: str
+    is_point: bool = False
+    point: tuple = (0.0, 0.0)
+    polygons: list = None
+    density: float = 1.0
+
+
+class Regions:
+    """A region table plus each event's region, resident on one GPU for the
+    location sampler (hk_regions_*): one uniform draw per event from its
+    region, Philox-keyed by (seed, counter) -- the reference's algorithm
+    (sample_point_in_region, geo.hpp:138-161) on its own random stream."""
+
+    def __init__(self, regions, event_region, device: int = 0):
+        is_point, pts, rparts, prings, rverts, verts, ids = [], [], [0], [0], [0], [], []
+        for r in regions:
+            is_point.append(1 if r.is_point else 0)
+            pts.extend([float(r.point[0]), float(r.point[1])])
+            ids.append(r.id.encode())
+            for poly in (r.polygons or []):
+                for ring in poly:
+                    ring = np.asarray(ring, dtype=np.float64).reshape(-1, 2)
+                    verts.append(ring)
+                    rverts.append(rverts[-1] + len(ring))
+                prings.append(prings[-1] + len(poly))
+            rparts.append(len(prings) - 1)
+        self._ids = (C.c_char_p * len(ids))(*ids)
+        er = np.ascontiguousarray(event_region, dtype=np.int32)
+        self.n_events = len(er)
+        h = C.c_void_p()
+        check(lib.hk_regions_create(
+            len(regions), np.ascontiguousarray(is_point, dtype=np.int32), np.ascontiguousarray(pts, dtype=np.float64),
+            np.ascontiguousarray(rparts, dtype=np.uintp), np.ascontiguousarray(prings, dtype=np.uintp),
+            np.ascontiguousarray(rverts, dtype=np.uintp),
+            np.ascontiguousarray(np.concatenate(verts) if verts else np.zeros((0, 2))).reshape(-1),
+            C.cast(self._ids, C.c_void_p), len(er), er, device, C.byref(h)))
+        self._h = h
+        self._fin = weakref.finalize(self, lib.hk_regions_destroy, h)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def sample(self, seed: int, counter: int = 0):
+        """One draw per event: (lon, lat) host arrays."""
+        lon, lat = np.zeros(self.n_events), np.zeros(self.n_events)
+        check(lib.hk_regions_sample(self._h, seed, counter, lon, lat))
+        return lon, lat
 
 
 class LikelihoodWorkspace:

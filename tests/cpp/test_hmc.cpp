@@ -230,9 +230,60 @@ void loglik_trace_matches_locations() {
              " rejected after a refresh, worst rel diff " + std::to_string(worst));
 }
 
+// HmcConfig::gpu_resample: X drawn on the GPU (Philox keyed by (seed,
+// refresh index)) straight into the engine.  Replaying the same draws
+// through b200::GpuRegions::sample must reproduce every loglik_trace entry,
+// and every draw must lie in its event's square.
+void gpu_resample_chain() {
+  const PointSetup setup = square_regions(simulated(), 4);
+  b200::HmcConfig cfg;
+  cfg.chain = base_config(setup.tagged);
+  cfg.chain.initial.variant = Variant::varying;
+  cfg.chain.iterations = 40;
+  cfg.chain.burn_in = 10;
+  cfg.chain.refresh_period = 1;
+  cfg.leapfrog_steps = 4;
+  cfg.step_size = 0.3;
+  cfg.adapt = false;
+  cfg.gpu_resample = true;
+  b200::HmcTiming timing;
+  const ChainOutput out = b200::run_cut_posterior_hmc(cfg, setup.tagged, setup.regions, &timing);
+  const b200::GpuRegions gpu(setup.tagged, setup.regions);
+  b200::Engine check(setup.tagged);
+  double worst = 0.0;
+  bool inside = true;
+  std::uint64_t refresh = 1;  // the constructor used refresh index 0
+  bool ok = out.loglik_trace.size() == out.draws.size();
+  for (std::size_t iter = 0; ok && iter < cfg.chain.iterations; ++iter) {
+    if (iter % cfg.chain.refresh_period == 0) {
+      auto [lon, lat] = gpu.sample(cfg.chain.seed, refresh++);
+      for (std::size_t e = 0; e < lon.size(); ++e)
+        inside = inside && setup.regions.at(setup.tagged[e].region_id).contains({lon[e], lat[e]});
+      check.set_locations(lon, lat);
+    }
+    if (iter < cfg.chain.burn_in) continue;
+    const std::size_t i = iter - cfg.chain.burn_in;
+    HawkesParams p = cfg.chain.initial;
+    p.mu0 = out.draws[i][0];
+    p.tau_t = out.draws[i][1];
+    p.xi0 = out.draws[i][2];
+    p.sigma_x = out.draws[i][3];
+    p.sigma_t = out.draws[i][4];
+    std::array<double, 5> g{};
+    const double want = check.log_likelihood_and_gradient(p, p.variant, g);
+    worst = std::max(worst, std::abs(out.loglik_trace[i] - want) / std::max(1.0, std::abs(want)));
+  }
+  ok = ok && inside && worst <= 1e-12;
+  char d[160];
+  std::snprintf(d, sizeof d, "%zu draws, all X in their squares: %d, worst rel diff %.3g, resample %.3f ms/refresh",
+                out.draws.size(), inside, worst, 1e3 * timing.resample_wait / cfg.chain.iterations);
+  report("cut-posterior HMC with GPU resample: trace == LL(draw i, replayed GPU X)", ok, d);
+}
+
 }  // namespace
 
 int main() {
+  gpu_resample_chain();
   loglik_trace_matches_locations();
   point_regions_collapse();
   posterior_agreement();

@@ -29,6 +29,7 @@ int main(int argc, char** argv) {
   const std::size_t iters = argc > 2 ? std::strtoull(argv[2], nullptr, 10) : 4;
   const int leapfrog = argc > 3 ? std::atoi(argv[3]) : 8;
   const int gpus = argc > 4 ? std::atoi(argv[4]) : 1;
+  const bool gpu_resample = argc > 5 && std::atoi(argv[5]) != 0;  // HmcConfig::gpu_resample
   constexpr int kGrid = 60;
   const double cell = 10.0 / kGrid;
   RegionTable regions;
@@ -68,17 +69,19 @@ int main(int argc, char** argv) {
   cfg.step_size = 1e-4;
   cfg.adapt = false;
   cfg.n_gpus = gpus;
+  cfg.gpu_resample = gpu_resample;
   b200::HmcSampler sampler(cfg, catalog, &regions);
   const ChainOutput out = sampler.run();
   const b200::HmcTiming& t = sampler.timing();
   const double per_iter = out.seconds / static_cast<double>(iters + 1);
   std::printf(
       "{\"config\": \"BASELINE config 5: cut-posterior HMC, county-uniform resample + density-scaled LL+grad\", "
-      "\"n_events\": %zu, \"counties\": %d, \"gpus\": %d, \"iterations\": %zu, \"leapfrog_steps\": %d, "
+      "\"n_events\": %zu, \"counties\": %d, \"gpus\": %d, \"gpu_resample\": %d, \"iterations\": %zu, "
+      "\"leapfrog_steps\": %d, "
       "\"seconds_per_iteration\": %.4f, \"evaluations\": %zu, \"seconds_per_evaluation\": %.4f, "
       "\"resample_wait_s_per_iter\": %.4f, \"set_locations_s_per_iter\": %.4f, "
       "\"reference_resample_s\": %.4f, \"accept_rate\": %.3f, \"final_loglik\": %.10g}\n",
-      n, kGrid * kGrid, gpus, iters + 1, leapfrog, per_iter, t.evaluations, t.evaluate / t.evaluations,
+      n, kGrid * kGrid, gpus, gpu_resample ? 1 : 0, iters + 1, leapfrog, per_iter, t.evaluations, t.evaluate / t.evaluations,
       t.resample_wait / (iters + 1), t.set_locations / (iters + 1), resample_s, out.acceptance_rate(0),
       sampler.loglik());
   return 0;
