@@ -210,7 +210,17 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
  *     pairs by the exact block expansion instead of
  *     per pair; 0 forces the direct per-pair path everywhere. */
 #define HK_OPT_BG_EXPANSION 1
+/*   HK_OPT_FGT: evaluate the homogeneous trigger of the tiles earlier than
+ *     each block's checkpoint by the certified Hermite expansion (fast Gauss
+ *     transform) where it is cheaper; 0 forces the
+ *     direct per-pair path.  Rows whose certified error bound could exceed
+ *     1e-13 relative make the synchronous calls recompute directly. */
+#define HK_OPT_FGT 2
 int hk_set_option(hk_ctx* ctx, int option, int value);
+/* Evaluations that used the Hermite expansion, synchronous ones recomputed
+ * directly after a failed certification, and whether the last asynchronous
+ * evaluation's certification failed (1; it is not recomputed). */
+int hk_fgt_stats(hk_ctx* ctx, long* evals, long* fallbacks, int* async_flagged);
 
 /* Rows [begin, end) this context evaluates, and its device count. */
 int hk_rows(const hk_ctx* ctx, size_t* begin, size_t* end, int* n_devices);
@@ -224,9 +234,10 @@ int hk_profile(hk_ctx* ctx, double* pair_kernel_ms, long* pair_launches, long* t
 int hk_reset_profile(hk_ctx* ctx);
 /* The same events split by launch kind: [0] pair launches computing both
  * halves, [1] background-only launches, [2] trigger-only launches (the
- * density-scaled plan runs one [1] and one [2] per evaluation).  ms3 and
- * launches3 have 3 entries each. */
-int hk_profile_kinds(hk_ctx* ctx, double* ms3, long* launches3);
+ * density-scaled plan runs one [1] and one [2] per evaluation), [3] the
+ * Hermite expansion's moment launches (box assignment, increments, scan),
+ * [4] its row evaluation.  ms5 and launches5 have 5 entries each. */
+int hk_profile_kinds(hk_ctx* ctx, double* ms5, long* launches5);
 
 /* Catalog invariants (types.hpp:43-57) and HawkesParams::validate
  * (types.hpp:92-103) on their own, with the reference's messages. */

@@ -26,6 +26,7 @@ lib = C.CDLL(str(LIB_PATH))
 
 HK_OK, HK_INVALID_ARGUMENT, HK_OUT_OF_RANGE, HK_RUNTIME_ERROR, HK_NOT_IMPLEMENTED = range(5)
 HK_OPT_BG_EXPANSION = 1
+HK_OPT_FGT = 2
 
 
 class hk_params(C.Structure):
@@ -68,6 +69,7 @@ SIGNATURES = [
     ("hk_resample_locations", C.c_int, [_ctx, C.c_void_p, C.c_uint64, C.c_uint64]),
     ("hk_eval_rows", C.c_int, [_ctx, _pp, _sz, _sz, _dp, C.c_void_p]),
     ("hk_set_option", C.c_int, [_ctx, C.c_int, C.c_int]),
+    ("hk_fgt_stats", C.c_int, [_ctx, C.POINTER(C.c_long), C.POINTER(C.c_long), C.POINTER(C.c_int)]),
     ("hk_rows", C.c_int, [_ctx, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int)]),
     ("hk_set_profiling", C.c_int, [_ctx, C.c_int]),
     ("hk_profile", C.c_int, [_ctx, C.POINTER(C.c_double), C.POINTER(C.c_long), C.POINTER(C.c_long)]),

@@ -32,6 +32,7 @@
 #include "../../include/hawkes_b200.h"
 #include "hk_device.cuh"
 #include "hk_host.hpp"
+#include "hk_fgt.cuh"
 #include "hk_kernels.cuh"
 #include "hk_regions.hpp"
 
@@ -166,11 +167,23 @@ struct DeviceState {
   int n_finish_blocks = 0;
   double* out6 = nullptr;
   double* h_out6 = nullptr;  // pinned
+  // Hermite expansion of the homogeneous trigger (hk_fgt.cu): checkpoint
+  // prefixes of this shard's row blocks and the per-evaluation buffers
+  int nck = 0, fgt_cols = 0;
+  double fgt_direct_cost = 0.0;  // trigger pairs the expansion replaces (sum over rows of P_k)
+  int* ck_P = nullptr;                                   // [nck]
+  double *fgt_tR = nullptr, *fgt_decay = nullptr, *fgt_dt = nullptr;  // [nck]
+  int* fgt_box = nullptr;                                // [fgt_cols]
+  double *fgt_u = nullptr, *fgt_v = nullptr;             // [fgt_cols]
+  double* fgt_mom = nullptr;                             // [nck][nbox][2][P^2], grown on demand
+  std::size_t fgt_mom_bytes = 0;
+  unsigned* fgt_flag = nullptr;                          // device
+  unsigned* h_fgt_flag = nullptr;                        // pinned
   double* gather6 = nullptr;  // [n_dev][6]: every device's out6 (multi-device contexts)
   double* total6 = nullptr;   // their device-order sum
   cudaEvent_t done = nullptr; // peer-copy mode: this device's part is ready
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
-  std::vector<int> prof_kind;  // per used event pair: 0 both halves, 1 background, 2 trigger
+  std::vector<int> prof_kind;  // per used event pair: 0 both halves, 1 background, 2 trigger, 3 FGT moments, 4 FGT rows
   std::size_t prof_used = 0;
 
   hk::DeviceCatalog catalog(int n, int npad) const {
@@ -198,6 +211,16 @@ struct hk_ctx {
   double* h_bbox = nullptr;        // pinned
   bool profiling = false;
   int bg_expansion = 1;
+  int fgt_enabled = 1;  // HK_OPT_FGT
+  long fgt_evals = 0, fgt_fallbacks = 0;
+  bool fgt_pending = false;  // an async evaluation's certification flag is unread
+
+  // Per-evaluation decision for the homogeneous trigger's Hermite expansion.
+  struct FgtPlan {
+    bool on = false;
+    int nb = 0;
+    double L = 0, x0 = 0, y0 = 0, inv_sqd = 0, delta = 0, eps = 0;
+  };
 
   // Workspace cache keys (LikelihoodWorkspace semantics, engine.hpp:117-229):
   // the background half depends on tau_t only, the trigger half on
@@ -244,6 +267,11 @@ struct hk_ctx {
       for (hk::Item* it : s.items)
         if (it) cudaFree(it);
       if (s.h_out6) cudaFreeHost(s.h_out6);
+      for (void* q : {static_cast<void*>(s.ck_P), static_cast<void*>(s.fgt_tR), static_cast<void*>(s.fgt_decay),
+                      static_cast<void*>(s.fgt_dt), static_cast<void*>(s.fgt_box), static_cast<void*>(s.fgt_u),
+                      static_cast<void*>(s.fgt_v), static_cast<void*>(s.fgt_mom), static_cast<void*>(s.fgt_flag)})
+        if (q) cudaFree(q);
+      if (s.h_fgt_flag) cudaFreeHost(s.h_fgt_flag);
       if (s.gather6) cudaFree(s.gather6);
       if (s.total6) cudaFree(s.total6);
       if (s.done) cudaEventDestroy(s.done);
@@ -419,6 +447,28 @@ struct hk_ctx {
          "upload items");
     }
     const std::size_t rows = static_cast<std::size_t>(re - rb);
+    {  // Hermite-expansion checkpoints of the homogeneous plan (hk_host.cpp plan_items: Item::xt)
+      static_assert(hk::kFgtRowBlock == hk::rows_per_item(false), "FGT checkpoints follow the homogeneous plan");
+      const int bi = hk::rows_per_item(false);
+      const int nblocks = (re - rb + bi - 1) / bi;
+      s.nck = (nblocks + hk::kFgtBlocks - 1) / hk::kFgtBlocks;
+      std::vector<int> ckp(s.nck);
+      for (int k = 0; k < s.nck; ++k) ckp[k] = lb[rb + k * hk::kFgtBlocks * bi] / hk::kBJ * hk::kBJ;
+      s.fgt_cols = s.nck ? ckp.back() : 0;
+      s.ck_P = dmalloc<int>(s.nck);
+      ck(cudaMemcpy(s.ck_P, ckp.data(), s.nck * sizeof(int), cudaMemcpyHostToDevice), "upload checkpoints");
+      s.fgt_tR = dmalloc<double>(s.nck);
+      s.fgt_decay = dmalloc<double>(s.nck);
+      s.fgt_dt = dmalloc<double>(s.nck);
+      s.fgt_box = dmalloc<int>(s.fgt_cols);
+      s.fgt_u = dmalloc<double>(s.fgt_cols);
+      s.fgt_v = dmalloc<double>(s.fgt_cols);
+      s.fgt_flag = dmalloc<unsigned>(1);
+      ck(cudaMallocHost(&s.h_fgt_flag, sizeof(unsigned)), "cudaMallocHost");
+      s.fgt_direct_cost = 0.0;
+      for (int b = 0; b < nblocks; ++b)
+        s.fgt_direct_cost += static_cast<double>(std::min(bi, re - rb - b * bi)) * ckp[b / hk::kFgtBlocks];
+    }
     s.partial = dmalloc<double>(static_cast<std::size_t>(std::max(s.slots[0], s.slots[1])) * 5 * rows);
     for (int k = 0; k < 2; ++k) {
       s.bg_sums[k] = dmalloc<double>(2 * rows);
@@ -477,13 +527,87 @@ struct hk_ctx {
     return c;
   }
 
+  // Whether this evaluation's homogeneous trigger goes through the Hermite
+  // expansion: homogeneous FP64, expansion enabled, a box grid of at most
+  // kFgtMaxBoxes boxes of side sqrt(2) sqrt(2 sigma_x^2), and an expected
+  // cost (rows x boxes x terms) below half the direct trigger pairs it
+  // replaces (x 16 FP64 each).
+  FgtPlan fgt_plan(const hk::EvalCoef& c, bool grad) const {
+    FgtPlan f;
+    if (!fgt_enabled || c.varying || c.single_prec || !locations_valid) return f;
+    const double sqd = std::sqrt(2.0) * c.sigma_x;
+    const double L = hk::kFgtGamma * sqd;
+    const double span = 2.0 * half_extent;
+    const double nbd = std::max(1.0, std::ceil(span / L));
+    if (!(nbd * nbd <= hk::kFgtMaxBoxes)) return f;
+    const int nb = static_cast<int>(nbd);
+    double direct = 0.0, expanded = 0.0;
+    const double per_row = static_cast<double>(nb * nb) * hk::kFgtP * hk::kFgtP * (grad ? 3.0 : 1.0);
+    std::size_t moments = 0;
+    for (const auto& s : devs) {
+      direct += 16.0 * s.fgt_direct_cost;
+      expanded += per_row * (s.re - s.rb);
+      moments = std::max(moments, static_cast<std::size_t>(s.nck) * nb * nb * 2 * hk::kFgtP * hk::kFgtP);
+    }
+    if (!(expanded < 0.5 * direct) || moments * sizeof(double) > (std::size_t{6} << 30)) return f;
+    f.on = true;
+    f.nb = nb;
+    f.L = L;
+    f.x0 = cx - 0.5 * nb * L;
+    f.y0 = cy - 0.5 * nb * L;
+    f.inv_sqd = 1.0 / sqd;
+    f.delta = 2.0 * c.sigma_x * c.sigma_x;
+    f.eps = hk::fgt_truncation_bound(hk::kFgtP, hk::kFgtGamma) + 4e-16;  // + rounding of the sums
+    return f;
+  }
+
+  hk::FgtParams fgt_params(DeviceState& s, const hk::EvalCoef& c, const FgtPlan& f, bool grad) {
+    const std::size_t need = static_cast<std::size_t>(s.nck) * f.nb * f.nb * 2 * hk::kFgtP * hk::kFgtP *
+                             sizeof(double);
+    if (need > s.fgt_mom_bytes) {
+      if (s.fgt_mom) ck(cudaFree(s.fgt_mom), "cudaFree");
+      s.fgt_mom = nullptr;
+      s.fgt_mom_bytes = 0;
+      s.fgt_mom = dmalloc<double>(need / sizeof(double));
+      s.fgt_mom_bytes = need;
+    }
+    hk::FgtParams F{};
+    F.n = n;
+    F.ncols = s.fgt_cols;
+    F.t = s.t;
+    F.x = s.x;
+    F.y = s.y;
+    F.nck = s.nck;
+    F.P = s.ck_P;
+    F.tR = s.fgt_tR;
+    F.decay = s.fgt_decay;
+    F.dt = s.fgt_dt;
+    F.nb = f.nb;
+    F.nbox = f.nb * f.nb;
+    F.x0 = f.x0;
+    F.y0 = f.y0;
+    F.L = f.L;
+    F.inv_sqd = f.inv_sqd;
+    F.omega = c.omega;
+    F.delta = f.delta;
+    F.eps = f.eps;
+    F.row_tol = hk::kFgtRowTol;
+    if (const char* e = std::getenv("HK_FGT_ROW_TOL")) F.row_tol = std::atof(e);  // tests: force the fallback
+    F.grad = grad ? 1 : 0;
+    F.box = s.fgt_box;
+    F.u = s.fgt_u;
+    F.v = s.fgt_v;
+    F.mom = s.fgt_mom;
+    return F;
+  }
+
   // The trigger half depends on the variant and on the precision.
   static int tr_variant(const hk::EvalCoef& c) { return c.varying + 2 * c.single_prec; }
 
   // Picks the cache entry for each half: a hit (unless forced) or the least
   // recently used entry, which the next enqueue recomputes.  Returns the
   // halves to compute.
-  int plan_halves(const hk::EvalCoef& c, bool grad, bool force, int& bgi, int& tri) {
+  int plan_halves(const hk::EvalCoef& c, bool grad, bool force, int& bgi, int& tri, bool fgt = false) {
     // the background half is FP64 in both precisions, but each precision
     // keeps its own entries so a cached result is bitwise the fresh one of
     // the same precision (the launches differ between the two)
@@ -493,7 +617,7 @@ struct hk_ctx {
     };
     auto hit_tr = [&](const Key& k) {
       return k.valid && k.a == c.sigma_x && k.b == c.sigma_t && k.variant == tr_variant(c) &&
-             k.loc == loc_version && (k.grad || !grad);
+             k.loc == loc_version && k.bgx == (fgt ? 1 : 0) && (k.grad || !grad);
     };
     int halves = 0;
     bgi = -1;
@@ -512,7 +636,7 @@ struct hk_ctx {
     if (tri < 0) {
       halves |= hk::kHalfTr;
       tri = tr_key[0].used <= tr_key[1].used ? 0 : 1;
-      tr_key[tri] = Key{true, c.sigma_x, c.sigma_t, tr_variant(c), grad ? 1 : 0, 0, loc_version, 0};
+      tr_key[tri] = Key{true, c.sigma_x, c.sigma_t, tr_variant(c), grad ? 1 : 0, fgt ? 1 : 0, loc_version, 0};
     }
     bg_key[bgi].used = ++clock;
     tr_key[tri].used = ++clock;
@@ -524,7 +648,7 @@ struct hk_ctx {
   // ell_rows / grad_rows (device, optional): the shard's per-row ell_n and
   // d ell_n / d theta from the same launches.
   void enqueue(DeviceState& s, const hk::EvalCoef& c, bool grad, int halves, int bgi, int tri,
-               double* ell_rows = nullptr, double* grad_rows = nullptr) {
+               double* ell_rows = nullptr, double* grad_rows = nullptr, const FgtPlan* fgt = nullptr) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const hk::DeviceCatalog dc = s.catalog(n, npad);
     const int rows = s.re - s.rb;
@@ -535,6 +659,13 @@ struct hk_ctx {
                          32 * hk::rows_per_thread(true), c.cx, c.cy, half_extent, s.stream);
       s.rperm_loc = loc_version;
       prof_total += 1;
+    }
+    const bool use_fgt = fgt && fgt->on && (halves & hk::kHalfTr) && s.nck > 0;
+    hk::FgtParams F{};
+    if (use_fgt) {
+      F = fgt_params(s, c, *fgt, grad);
+      timed_pair(s, 3, [&] { hk::launch_fgt_prepare(F, s.stream); });
+      prof_total += 4;
     }
     if (halves) {
       hk::launch_prep(dc, c, s.stream);
@@ -564,7 +695,8 @@ struct hk_ctx {
       } else {
         const int kind = halves == (hk::kHalfBg | hk::kHalfTr) ? 0 : (halves == hk::kHalfBg ? 1 : 2);
         timed_pair(s, kind, [&] {
-          hk::launch_pair(dc, c, s.items[v], s.n_items[v], s.partial, s.rb, rows, grad, halves, s.stream);
+          hk::launch_pair(dc, c, s.items[v], s.n_items[v], s.partial, s.rb, rows, grad, halves, s.stream,
+                          use_fgt);
         });
       }
       if (split) {
@@ -581,6 +713,15 @@ struct hk_ctx {
       }
       if (profiling) prof_pair += 1;
     }
+    if (use_fgt) {
+      ck(cudaMemsetAsync(s.fgt_flag, 0, sizeof(unsigned), s.stream), "memset");
+      timed_pair(s, 4, [&] {
+        hk::launch_fgt_eval(F, s.rb, rows, s.bg_sums[bgi], s.tr_sums[tri], c.a, c.c, s.fgt_flag, s.stream);
+      });
+      ck(cudaMemcpyAsync(s.h_fgt_flag, s.fgt_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, s.stream),
+         "flag copy");
+      prof_total += 1;
+    }
     hk::launch_finish(dc, c, s.bg_sums[bgi], s.tr_sums[tri], s.rb, rows, grad, ell_rows,
                       grad ? grad_rows : nullptr, s.blockpart, s.stream);
     hk::launch_reduce(s.blockpart, s.n_finish_blocks, s.out6, s.stream);
@@ -592,11 +733,13 @@ struct hk_ctx {
   // ell_rows / grad_rows (host, optional): per-row outputs of the context's
   // rows, devices in order (hk_eval_detail).
   void evaluate(const hk_params* p, bool grad, bool workspace, bool force, double* ll, double* grad5,
-                bool single = false, double* ell_rows = nullptr, double* grad_rows = nullptr) {
+                bool single = false, double* ell_rows = nullptr, double* grad_rows = nullptr,
+                bool allow_fgt = true) {
     const hk::EvalCoef c = coef(p, single);
+    const FgtPlan fgt = allow_fgt ? fgt_plan(c, grad) : FgtPlan{};
     int bgi, tri;
-    const int halves = workspace ? plan_halves(c, grad, force, bgi, tri)
-                                 : plan_halves(c, grad, /*force=*/true, bgi, tri);
+    const int halves = workspace ? plan_halves(c, grad, force, bgi, tri, fgt.on)
+                                 : plan_halves(c, grad, /*force=*/true, bgi, tri, fgt.on);
     std::vector<double*> dev_rows(devs.size(), nullptr);
     struct Free {
       std::vector<double*>& v;
@@ -616,7 +759,7 @@ struct hk_ctx {
         d_ell = dev_rows[k];
         d_grad = dev_rows[k] + rows;
       }
-      enqueue(s, c, grad, halves, bgi, tri, d_ell, d_grad);
+      enqueue(s, c, grad, halves, bgi, tri, d_ell, d_grad, &fgt);
       if (devs.size() == 1)
         ck(cudaMemcpyAsync(s.h_out6, s.out6, 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
            "result copy");
@@ -637,9 +780,20 @@ struct hk_ctx {
                          devs[0].stream),
          "result copy");
     }
+    bool flagged = false;
     for (auto& s : devs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       ck(cudaStreamSynchronize(s.stream), "hk_eval");
+      if (fgt.on && (halves & hk::kHalfTr) && s.nck > 0) flagged = flagged || *s.h_fgt_flag != 0;
+    }
+    if (fgt.on && (halves & hk::kHalfTr)) ++fgt_evals;
+    if (flagged) {
+      // a row's certified expansion error could exceed kFgtRowTol: the same
+      // evaluation on the direct path (both halves recomputed, caches reset)
+      ++fgt_fallbacks;
+      for (Key& k : tr_key) k.valid = false;
+      evaluate(p, grad, workspace, /*force=*/true, ll, grad5, single, ell_rows, grad_rows, /*allow_fgt=*/false);
+      return;
     }
     const double* acc = devs[0].h_out6;
     *ll = acc[0];
@@ -988,9 +1142,14 @@ int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("hk_eval_async: null context");
     const hk::EvalCoef c = ctx->coef(p);
+    const hk_ctx::FgtPlan fgt = ctx->fgt_plan(c, with_grad != 0);
     int bgi, tri;
-    const int halves = ctx->plan_halves(c, with_grad != 0, /*force=*/true, bgi, tri);
-    for (auto& s : ctx->devs) ctx->enqueue(s, c, with_grad != 0, halves, bgi, tri);
+    const int halves = ctx->plan_halves(c, with_grad != 0, /*force=*/true, bgi, tri, fgt.on);
+    for (auto& s : ctx->devs) ctx->enqueue(s, c, with_grad != 0, halves, bgi, tri, nullptr, nullptr, &fgt);
+    if (fgt.on) {
+      ++ctx->fgt_evals;
+      ctx->fgt_pending = true;
+    }
     if (ctx->devs.size() > 1) ctx->reduce_devices();
   });
 }
@@ -1068,10 +1227,28 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
   });
 }
 
+int hk_fgt_stats(hk_ctx* ctx, long* evals, long* fallbacks, int* async_flagged) {
+  return guarded([&] {
+    if (!ctx) throw std::invalid_argument("hk_fgt_stats: null context");
+    int flagged = 0;
+    if (ctx->fgt_pending) {
+      for (auto& s : ctx->devs) {
+        ck(cudaSetDevice(s.dev), "cudaSetDevice");
+        ck(cudaStreamSynchronize(s.stream), "hk_fgt_stats");
+        if (s.nck > 0 && *s.h_fgt_flag) flagged = 1;
+      }
+    }
+    if (evals) *evals = ctx->fgt_evals;
+    if (fallbacks) *fallbacks = ctx->fgt_fallbacks;
+    if (async_flagged) *async_flagged = flagged;
+  });
+}
+
 int hk_set_option(hk_ctx* ctx, int option, int value) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("hk_set_option: null context");
     if (option == HK_OPT_BG_EXPANSION) ctx->bg_expansion = value != 0;
+    else if (option == HK_OPT_FGT) ctx->fgt_enabled = value != 0;
     else throw std::invalid_argument("hk_set_option: unknown option " + std::to_string(option));
   });
 }
@@ -1112,12 +1289,12 @@ int hk_profile(hk_ctx* ctx, double* pair_kernel_ms, long* pair_launches, long* t
   });
 }
 
-int hk_profile_kinds(hk_ctx* ctx, double* ms3, long* launches3) {
+int hk_profile_kinds(hk_ctx* ctx, double* ms5, long* launches5) {
   return guarded([&] {
-    if (!ctx || !ms3 || !launches3) throw std::invalid_argument("hk_profile_kinds: null argument");
-    for (int k = 0; k < 3; ++k) {
-      ms3[k] = 0.0;
-      launches3[k] = 0;
+    if (!ctx || !ms5 || !launches5) throw std::invalid_argument("hk_profile_kinds: null argument");
+    for (int k = 0; k < 5; ++k) {
+      ms5[k] = 0.0;
+      launches5[k] = 0;
     }
     for (auto& s : ctx->devs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
@@ -1126,8 +1303,8 @@ int hk_profile_kinds(hk_ctx* ctx, double* ms3, long* launches3) {
         float m = 0.f;
         ck(cudaEventElapsedTime(&m, s.prof_events[i].first, s.prof_events[i].second),
            "cudaEventElapsedTime");
-        ms3[s.prof_kind[i]] += m;
-        launches3[s.prof_kind[i]] += 1;
+        ms5[s.prof_kind[i]] += m;
+        launches5[s.prof_kind[i]] += 1;
       }
     }
   });

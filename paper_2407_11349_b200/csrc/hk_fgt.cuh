@@ -1,0 +1,45 @@
+// Launch-side view of the homogeneous-trigger Hermite expansion (hk_fgt.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace hk {
+
+constexpr int kFgtP = 30;              // Hermite terms per dimension (a, b < kFgtP)
+constexpr double kFgtGamma = 1.4142135623730951;  // box side / sqrt(delta): rho = 1
+constexpr int kFgtBlocks = 4;          // homogeneous row blocks per checkpoint
+constexpr int kFgtRowBlock = 512;      // rows per block of the homogeneous plan (rows_per_item(false))
+constexpr int kFgtEvalThreads = 128;   // rows per evaluation CTA (divides kFgtRowBlock)
+constexpr double kFgtCut = 46.0;       // boxes farther than sqrt(46) scaled units are skipped
+constexpr double kFgtRowTol = 1e-13;   // certified per-row relative error bound, else recompute directly
+constexpr int kFgtMaxBoxes = 1024;     // larger grids (small sigma_x / wide catalogs): direct path
+
+struct FgtParams {
+  int n, ncols;                 // catalog size; columns below the last prefix
+  const double *t, *x, *y;
+  int nck;                      // checkpoints
+  const int* P;                 // [nck] prefix boundaries (columns [0, P_k)), nondecreasing
+  double* tR;                   // [nck] reference times t[P_k]
+  double* decay;                // [nck] exp(-omega (tR_k - tR_{k-1}))
+  double* dt;                   // [nck] tR_k - tR_{k-1}
+  int nb, nbox;                 // boxes per side, boxes
+  double x0, y0, L, inv_sqd;    // grid origin, box side, 1 / sqrt(delta)
+  double omega, delta;          // 1 / sigma_t, 2 sigma_x^2
+  double eps;                   // truncation bound per unit of box weight
+  double row_tol;               // certified per-row relative bound (kFgtRowTol)
+  int grad;
+  int* box;                     // [ncols]
+  double *u, *v;                // [ncols] scaled offsets from the box centre
+  double* mom;                  // [nck][nbox][2][kFgtP^2]: A (and B) moments
+};
+
+// eps_p of hk_fgt.cu for p terms and box side gamma sqrt(delta).
+double fgt_truncation_bound(int p, double gamma);
+// reference times, box assignment, increment moments and their scan.
+void launch_fgt_prepare(const FgtParams& F, cudaStream_t s);
+// adds the expansion's trigger sums into tr_sums (planes T, Td, Tq of
+// rows_total rows); sets *flag when a row's certified bound fails.
+void launch_fgt_eval(const FgtParams& F, int rows_base, int rows_total, const double* bg_sums,
+                     double* tr_sums, double coef_a, double coef_c, unsigned* flag, cudaStream_t s);
+
+}  // namespace hk

@@ -7,6 +7,7 @@
 #include <numeric>
 
 #include "hk_device.cuh"
+#include "hk_fgt.cuh"
 
 namespace hk {
 
@@ -209,6 +210,9 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
     const int w1 = G > 1 ? std::min(re, rb + window_first_block(w + 1, nblocks, nw) * kBI) : r1;
     const int pos = G > 1 ? w * G * kBI + (b - b0) * kBI : -1;
     const int lbmin = lb[w0], ubmax = ub[w1 - 1];
+    // Hermite-expansion checkpoint of this block (homogeneous plan): the
+    // prefix of whole tiles before the checkpoint's first row (hk_fgt.cu)
+    const int xt = G > 1 ? 0 : lb[rb + (b / kFgtBlocks) * kFgtBlocks * kBI] / kBJ;
     for (int c = 0; c < slots; ++c) {
       const int tb = c * per, te = std::min(ntiles, (c + 1) * per);
       double cost = 0.0;
@@ -219,7 +223,7 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
         else if (j0 >= ubmax && j1 <= n) cost += alpha;
         else cost += kCostAlphaDirect + kCostBeta + 8.0;
       }
-      cands.push_back({Item{w0, w1, tb, te, c, pos}, cost * (r1 - r0)});
+      cands.push_back({Item{w0, w1, tb, te, c, pos, xt}, cost * (r1 - r0)});
     }
   }
   std::stable_sort(cands.begin(), cands.end(),

@@ -92,47 +92,6 @@ enum CompactSlot { cXY = 0, cWK = 2, cVZ = 4, cT = 4, cQ = 5 };
 template <bool kC>
 constexpr int kStageSlots = kC ? 6 : kSlots;
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_fence_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "HK_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra HK_WAIT;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(phase)
-      : "memory");
-}
-
-// 1-D bulk async copy global -> shared (TMA engine; SASS UBLKCP).
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
 struct PairParams {
   DeviceCatalog d;
   EvalCoef c;
@@ -140,6 +99,7 @@ struct PairParams {
   double* partial;
   int rows_base, rows_total;
   int halves;  // kHalfBg | kHalfTr: which row sums this launch must produce
+  int fgt;     // trigger below Item::xt external (hk_fgt.cu)
 };
 
 struct BlockInfo {
@@ -681,7 +641,10 @@ __global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
   HK_ASSERT(ntl >= 0 && ntl <= kMaxItemTiles && it.te * kBJ <= P.d.npad);
   for (int k = tid; k < ntl; k += kThreads) {
     const int ta = tile_type_all(it.tb + k, bi, P);
-    s_cls[k] = static_cast<unsigned char>(restrict_type(ta, HK_HALVES) | (ta << 4));
+    // tiles below xt (all strictly earlier than the block's rows) keep only
+    // their background when the Hermite expansion supplies their trigger
+    const int tf = (P.fgt && it.tb + k < it.xt) ? restrict_type(ta, kHalfBg) : ta;
+    s_cls[k] = static_cast<unsigned char>(restrict_type(tf, HK_HALVES) | (ta << 4));
   }
   __syncthreads();
   // Unit sequence (warp-uniform state): runs of expansion tiles (full class
@@ -1156,9 +1119,9 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
                  double* partial, int rows_base, int rows_total, bool with_grad, int halves,
-                 cudaStream_t s) {
+                 cudaStream_t s, bool fgt) {
   if (n_items <= 0) return;
-  PairParams P{d, c, items, partial, rows_base, rows_total, halves};
+  PairParams P{d, c, items, partial, rows_base, rows_total, halves, fgt ? 1 : 0};
   if (halves == kHalfBg && !c.varying) {  // background only, homogeneous plan (FP64 either way)
     switch ((with_grad && !c.single_prec ? 3 : 0) + c.mode) {
       case 0: launch_pair_t<false, false, kExact, false, 1>(P, n_items, s); break;

@@ -16,6 +16,8 @@ namespace hk {
 // in which each warp's 32*NR consecutive positions form one cluster.
 struct Item {
   int rb, re, tb, te, slot, pos;
+  int xt;  // homogeneous plan: the trigger of tiles below xt comes from the Hermite expansion
+           // (hk_fgt.cu) when the launch says so (PairParams::fgt); 0 otherwise
 };
 constexpr int kMaxItemTiles = 2048;  // te - tb (the pair kernel classifies them in shared memory)
 // Work items per launch the planner aims for (~72 waves of 148 SMs x 3
@@ -102,9 +104,11 @@ __host__ __device__ inline int window_first_block(int w, int nblocks, int n_wind
 __host__ __device__ inline int window_of_block(int b, int nblocks, int n_windows) {
   return static_cast<int>((static_cast<long long>(b + 1) * n_windows - 1) / nblocks);
 }
+// fgt: the trigger of each item's tiles below Item::xt is left out (it is
+// added by the Hermite expansion, hk_fgt.cu); homogeneous plan only.
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
                  double* partial, int rows_base, int rows_total, bool with_grad, int halves,
-                 cudaStream_t s);
+                 cudaStream_t s, bool fgt = false);
 // Sums the partial slots per row (fixed order) into the background plane
 // pair [B, B2] and/or the trigger planes [T, Td, Tq] (either may be null).
 void launch_collapse(const double* partial, int slots, int rows_total, double* bg_sums,

@@ -289,6 +289,17 @@ class Evaluator:
         forces the direct per-pair path."""
         check(lib.hk_set_option(self._h, _lib.HK_OPT_BG_EXPANSION, int(on)))
 
+    def set_fgt(self, on: bool) -> None:
+        """HK_OPT_FGT: the homogeneous trigger's Hermite expansion (default on)."""
+        check(lib.hk_set_option(self._h, _lib.HK_OPT_FGT, int(on)))
+
+    def fgt_stats(self):
+        """(evaluations through the expansion, direct recomputations, last
+        async evaluation flagged)."""
+        e, f, a = C.c_long(), C.c_long(), C.c_int()
+        check(lib.hk_fgt_stats(self._h, C.byref(e), C.byref(f), C.byref(a)))
+        return e.value, f.value, bool(a.value)
+
     def set_profiling(self, on: bool) -> None:
         check(lib.hk_set_profiling(self._h, int(on)))
 
@@ -298,9 +309,10 @@ class Evaluator:
         return ms.value, npair.value, ntot.value
 
     def profile_kinds(self):
-        """(ms[3], launches[3]) of the pair launches by kind: both halves,
-        background only, trigger only."""
-        ms, n = np.zeros(3), np.zeros(3, dtype=np.int64)
+        """(ms[5], launches[5]) of the pair launches by kind: both halves,
+        background only, trigger only, Hermite-expansion moments, Hermite-
+        expansion rows."""
+        ms, n = np.zeros(5), np.zeros(5, dtype=np.int64)
         check(lib.hk_profile_kinds(self._h, ms, n))
         return ms, n
 

@@ -10,7 +10,8 @@ Workloads (benchmark_catalog(N, 42), bench params, LL + gradient):
   constant  the homogeneous evaluation: one pair launch computing both halves
   varying   the density-scaled evaluation: a background-only launch of the
             homogeneous kernel + the trigger-only density-scaled launch
-  direct    constant with the background block expansion off
+  direct    constant with the background block expansion and the trigger's
+            Hermite expansion off (the pure O(N^2) pair kernel)
 """
 import csv
 import hashlib
@@ -36,10 +37,14 @@ def worker(n, mode):
                      variant=Variant.varying if mode == "varying" else Variant.constant)
     if mode == "direct":
         ev.set_bg_expansion(False)
+        ev.set_fgt(False)
     ev.eval(p, grad=True)
 
 
 def kind_of(name):
+    if "fgt_" in name:  # the Hermite expansion's launches (hk_fgt.cu)
+        base = name.split("fgt_", 1)[1].split("_kernel", 1)[0]
+        return {"eval": "fgt_rows"}.get(base, "fgt_" + base)
     # pair_kernel<kVarying, kGrad, kMode, kF32, kOnly>
     args = name.split("pair_kernel<", 1)[1].split(">", 1)[0].split(",")
     only = int(args[4]) if len(args) > 4 else 0
@@ -58,7 +63,7 @@ def main():
     for mode in ("constant", "varying", "direct"):
         csv_path = log / f"counts_{mode}.csv"
         subprocess.run(["ncu", "--metrics", ",".join(METRICS), "--clock-control", "none", "--print-units", "base", "-k",
-                        "regex:pair_kernel", "--csv", "--log-file", str(csv_path), sys.executable, __file__,
+                        "regex:pair_kernel|fgt_", "--csv", "--log-file", str(csv_path), sys.executable, __file__,
                         "--worker", str(n), mode], check=True, cwd=ROOT)
         rows = [r for r in csv.DictReader(l for l in csv_path.read_text().splitlines()
                                           if l.startswith('"'))]
@@ -77,6 +82,17 @@ def main():
                 "dram_read_bytes": m["dram__bytes_read.sum"], "dram_write_bytes": m["dram__bytes_write.sum"],
                 "fp64_pipe_pct": m["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"],
                 "sm_clock_hz": m["sm__cycles_elapsed.avg.per_second"]}
+    # algorithmic bytes of the expansion's row launch: every checkpoint's
+    # prefix moments once (A and B sets, kFgtP^2 each, per box)
+    import math
+    from paper_2407_11349_b200 import benchmark_catalog
+    cat = benchmark_catalog(n, 42)
+    extent = max(cat.lon.max() - cat.lon.min(), cat.lat.max() - cat.lat.min())
+    nb = max(1, math.ceil(extent / (math.sqrt(2.0) * math.sqrt(2.0) * 0.5)))
+    nck = math.ceil(math.ceil(n / 512) / 4)
+    for tag, c in out["launches"].items():
+        if tag.endswith("_fgt_rows"):
+            c["moment_bytes"] = nck * nb * nb * 2 * 30 * 30 * 8
     OUT.write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps(out, indent=1))
 
