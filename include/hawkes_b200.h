@@ -216,8 +216,13 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
  *     direct per-pair path.  Rows whose certified error bound could exceed
  *     1e-13 relative make the synchronous calls recompute directly. */
 #define HK_OPT_FGT 2
+/*   HK_OPT_BG_FGT: evaluate the background sums of every row by the
+ *     certified 1-D Hermite expansion in time (both variants, FP64 only);
+ *     0 returns them to the pair kernels (block expansion / per pair). */
+#define HK_OPT_BG_FGT 3
 int hk_set_option(hk_ctx* ctx, int option, int value);
-/* Evaluations that used the Hermite expansion, synchronous ones recomputed
+/* Evaluations that used a Hermite expansion (trigger or background),
+ * synchronous ones recomputed
  * directly after a failed certification, and whether the last asynchronous
  * evaluation's certification failed (1; it is not recomputed). */
 int hk_fgt_stats(hk_ctx* ctx, long* evals, long* fallbacks, int* async_flagged);

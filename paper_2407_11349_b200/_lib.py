@@ -27,6 +27,7 @@ lib = C.CDLL(str(LIB_PATH))
 HK_OK, HK_INVALID_ARGUMENT, HK_OUT_OF_RANGE, HK_RUNTIME_ERROR, HK_NOT_IMPLEMENTED = range(5)
 HK_OPT_BG_EXPANSION = 1
 HK_OPT_FGT = 2
+HK_OPT_BG_FGT = 3
 
 
 class hk_params(C.Structure):

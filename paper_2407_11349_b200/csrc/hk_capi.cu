@@ -177,8 +177,12 @@ struct DeviceState {
   double *fgt_u = nullptr, *fgt_v = nullptr;             // [fgt_cols]
   double* fgt_mom = nullptr;                             // [nck][nbox][2][P^2], grown on demand
   std::size_t fgt_mom_bytes = 0;
+  double* bgf_mom = nullptr;  // [nbt][kFgtP]: the background's 1-D expansion
+  int* bgf_count = nullptr;   // [nbt]
+  int bgf_cap = 0;            // boxes allocated
   unsigned* fgt_flag = nullptr;                          // device
   unsigned* h_fgt_flag = nullptr;                        // pinned
+  bool flag_pending = false;                             // set by hk_eval_async
   double* gather6 = nullptr;  // [n_dev][6]: every device's out6 (multi-device contexts)
   double* total6 = nullptr;   // their device-order sum
   cudaEvent_t done = nullptr; // peer-copy mode: this device's part is ready
@@ -211,7 +215,8 @@ struct hk_ctx {
   double* h_bbox = nullptr;        // pinned
   bool profiling = false;
   int bg_expansion = 1;
-  int fgt_enabled = 1;  // HK_OPT_FGT
+  int fgt_enabled = 1;     // HK_OPT_FGT
+  int bg_fgt_enabled = 1;  // HK_OPT_BG_FGT
   long fgt_evals = 0, fgt_fallbacks = 0;
   bool fgt_pending = false;  // an async evaluation's certification flag is unread
 
@@ -220,6 +225,10 @@ struct hk_ctx {
     bool on = false;
     int nb = 0;
     double L = 0, x0 = 0, y0 = 0, inv_sqd = 0, delta = 0, eps = 0;
+    // the background's 1-D expansion in time
+    bool bg = false;
+    int nbt = 0;
+    double t0 = 0, Lt = 0, inv_sqdt = 0, delta_t = 0, eps_t = 0;
   };
 
   // Workspace cache keys (LikelihoodWorkspace semantics, engine.hpp:117-229):
@@ -269,7 +278,8 @@ struct hk_ctx {
       if (s.h_out6) cudaFreeHost(s.h_out6);
       for (void* q : {static_cast<void*>(s.ck_P), static_cast<void*>(s.fgt_tR), static_cast<void*>(s.fgt_decay),
                       static_cast<void*>(s.fgt_dt), static_cast<void*>(s.fgt_box), static_cast<void*>(s.fgt_u),
-                      static_cast<void*>(s.fgt_v), static_cast<void*>(s.fgt_mom), static_cast<void*>(s.fgt_flag)})
+                      static_cast<void*>(s.fgt_v), static_cast<void*>(s.fgt_mom), static_cast<void*>(s.fgt_flag),
+                      static_cast<void*>(s.bgf_mom), static_cast<void*>(s.bgf_count)})
         if (q) cudaFree(q);
       if (s.h_fgt_flag) cudaFreeHost(s.h_fgt_flag);
       if (s.gather6) cudaFree(s.gather6);
@@ -534,6 +544,21 @@ struct hk_ctx {
   // replaces (x 16 FP64 each).
   FgtPlan fgt_plan(const hk::EvalCoef& c, bool grad) const {
     FgtPlan f;
+    if (bg_fgt_enabled && !c.single_prec) {
+      // background: time boxes of side gamma sqrt(2 tau^2) over [t_0, t_end]
+      const double sqdt = std::sqrt(2.0) * c.tau_t;
+      const double Lt = hk::kFgtGamma * sqdt;
+      const double nbt = std::max(1.0, std::ceil((t[n - 1] - t[0]) / Lt));
+      if (nbt <= hk::kBgFgtMaxBoxes) {
+        f.bg = true;
+        f.nbt = static_cast<int>(nbt);
+        f.t0 = t[0];
+        f.Lt = Lt;
+        f.inv_sqdt = 1.0 / sqdt;
+        f.delta_t = 2.0 * c.tau_t * c.tau_t;
+        f.eps_t = hk::bg_fgt_truncation_bound(hk::kFgtP, hk::kFgtGamma) + 4e-16;
+      }
+    }
     if (!fgt_enabled || c.varying || c.single_prec || !locations_valid) return f;
     const double sqd = std::sqrt(2.0) * c.sigma_x;
     const double L = hk::kFgtGamma * sqd;
@@ -607,12 +632,14 @@ struct hk_ctx {
   // Picks the cache entry for each half: a hit (unless forced) or the least
   // recently used entry, which the next enqueue recomputes.  Returns the
   // halves to compute.
-  int plan_halves(const hk::EvalCoef& c, bool grad, bool force, int& bgi, int& tri, bool fgt = false) {
+  int plan_halves(const hk::EvalCoef& c, bool grad, bool force, int& bgi, int& tri, bool fgt = false,
+                  bool bg_fgt = false) {
+    const int bgx = c.bg_expansion + (bg_fgt ? 2 : 0);  // how the background half is computed
     // the background half is FP64 in both precisions, but each precision
     // keeps its own entries so a cached result is bitwise the fresh one of
     // the same precision (the launches differ between the two)
     auto hit_bg = [&](const Key& k) {
-      return k.valid && k.a == c.tau_t && k.b == c.single_prec && k.bgx == c.bg_expansion &&
+      return k.valid && k.a == c.tau_t && k.b == c.single_prec && k.bgx == bgx &&
              (k.grad || !grad);
     };
     auto hit_tr = [&](const Key& k) {
@@ -630,8 +657,7 @@ struct hk_ctx {
     if (bgi < 0) {
       halves |= hk::kHalfBg;
       bgi = bg_key[0].used <= bg_key[1].used ? 0 : 1;
-      bg_key[bgi] = Key{true, c.tau_t, static_cast<double>(c.single_prec), 0, grad ? 1 : 0,
-                        c.bg_expansion, 0, 0};
+      bg_key[bgi] = Key{true, c.tau_t, static_cast<double>(c.single_prec), 0, grad ? 1 : 0, bgx, 0, 0};
     }
     if (tri < 0) {
       halves |= hk::kHalfTr;
@@ -647,7 +673,9 @@ struct hk_ctx {
   // Enqueues [prep + pair + collapse for the missing halves] + finish + reduce.
   // ell_rows / grad_rows (device, optional): the shard's per-row ell_n and
   // d ell_n / d theta from the same launches.
-  void enqueue(DeviceState& s, const hk::EvalCoef& c, bool grad, int halves, int bgi, int tri,
+  // Returns whether an expansion ran (its certification flag is then copied
+  // to s.h_fgt_flag on the stream).
+  bool enqueue(DeviceState& s, const hk::EvalCoef& c, bool grad, int halves, int bgi, int tri,
                double* ell_rows = nullptr, double* grad_rows = nullptr, const FgtPlan* fgt = nullptr) {
     ck(cudaSetDevice(s.dev), "cudaSetDevice");
     const hk::DeviceCatalog dc = s.catalog(n, npad);
@@ -661,6 +689,38 @@ struct hk_ctx {
       prof_total += 1;
     }
     const bool use_fgt = fgt && fgt->on && (halves & hk::kHalfTr) && s.nck > 0;
+    const bool use_bgf = fgt && fgt->bg && (halves & hk::kHalfBg);
+    if (use_fgt || use_bgf) ck(cudaMemsetAsync(s.fgt_flag, 0, sizeof(unsigned), s.stream), "memset");
+    if (use_bgf) {  // the background half by the 1-D expansion in time, straight into bg_sums
+      if (fgt->nbt > s.bgf_cap) {
+        if (s.bgf_mom) ck(cudaFree(s.bgf_mom), "cudaFree");
+        if (s.bgf_count) ck(cudaFree(s.bgf_count), "cudaFree");
+        s.bgf_mom = nullptr;
+        s.bgf_count = nullptr;
+        s.bgf_cap = 0;
+        s.bgf_mom = dmalloc<double>(static_cast<std::size_t>(fgt->nbt) * hk::kFgtP);
+        s.bgf_count = dmalloc<int>(fgt->nbt);
+        s.bgf_cap = fgt->nbt;
+      }
+      hk::BgFgtParams G{};
+      G.n = n;
+      G.t = s.t;
+      G.lb = s.lb;
+      G.ub = s.ub;
+      G.nbt = fgt->nbt;
+      G.t0 = fgt->t0;
+      G.L = fgt->Lt;
+      G.inv_sqd = fgt->inv_sqdt;
+      G.delta = fgt->delta_t;
+      G.eps = fgt->eps_t;
+      G.row_tol = hk::kFgtRowTol;
+      if (const char* e = std::getenv("HK_FGT_ROW_TOL")) G.row_tol = std::atof(e);
+      G.mom = s.bgf_mom;
+      G.count = s.bgf_count;
+      timed_pair(s, 1, [&] { hk::launch_bg_fgt(G, s.rb, rows, s.bg_sums[bgi], s.fgt_flag, s.stream); });
+      prof_total += 2;
+      halves &= ~hk::kHalfBg;  // the pair kernels compute the trigger only
+    }
     hk::FgtParams F{};
     if (use_fgt) {
       F = fgt_params(s, c, *fgt, grad);
@@ -714,19 +774,20 @@ struct hk_ctx {
       if (profiling) prof_pair += 1;
     }
     if (use_fgt) {
-      ck(cudaMemsetAsync(s.fgt_flag, 0, sizeof(unsigned), s.stream), "memset");
       timed_pair(s, 4, [&] {
         hk::launch_fgt_eval(F, s.rb, rows, s.bg_sums[bgi], s.tr_sums[tri], c.a, c.c, s.fgt_flag, s.stream);
       });
-      ck(cudaMemcpyAsync(s.h_fgt_flag, s.fgt_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, s.stream),
-         "flag copy");
       prof_total += 1;
     }
+    if (use_fgt || use_bgf)
+      ck(cudaMemcpyAsync(s.h_fgt_flag, s.fgt_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, s.stream),
+         "flag copy");
     hk::launch_finish(dc, c, s.bg_sums[bgi], s.tr_sums[tri], s.rb, rows, grad, ell_rows,
                       grad ? grad_rows : nullptr, s.blockpart, s.stream);
     hk::launch_reduce(s.blockpart, s.n_finish_blocks, s.out6, s.stream);
     ck(cudaGetLastError(), "kernel launch");
     prof_total += 2;
+    return use_fgt || use_bgf;
   }
 
   // Full or workspace evaluation on every device; sums in device order.
@@ -738,8 +799,8 @@ struct hk_ctx {
     const hk::EvalCoef c = coef(p, single);
     const FgtPlan fgt = allow_fgt ? fgt_plan(c, grad) : FgtPlan{};
     int bgi, tri;
-    const int halves = workspace ? plan_halves(c, grad, force, bgi, tri, fgt.on)
-                                 : plan_halves(c, grad, /*force=*/true, bgi, tri, fgt.on);
+    const int halves = workspace ? plan_halves(c, grad, force, bgi, tri, fgt.on, fgt.bg)
+                                 : plan_halves(c, grad, /*force=*/true, bgi, tri, fgt.on, fgt.bg);
     std::vector<double*> dev_rows(devs.size(), nullptr);
     struct Free {
       std::vector<double*>& v;
@@ -749,6 +810,7 @@ struct hk_ctx {
       }
     } free_rows{dev_rows};
     std::size_t off = 0;
+    std::vector<char> expanded(devs.size(), 0);
     for (std::size_t k = 0; k < devs.size(); ++k) {
       auto& s = devs[k];
       const std::size_t rows = static_cast<std::size_t>(s.re - s.rb);
@@ -759,7 +821,7 @@ struct hk_ctx {
         d_ell = dev_rows[k];
         d_grad = dev_rows[k] + rows;
       }
-      enqueue(s, c, grad, halves, bgi, tri, d_ell, d_grad, &fgt);
+      expanded[k] = enqueue(s, c, grad, halves, bgi, tri, d_ell, d_grad, &fgt);
       if (devs.size() == 1)
         ck(cudaMemcpyAsync(s.h_out6, s.out6, 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
            "result copy");
@@ -780,18 +842,21 @@ struct hk_ctx {
                          devs[0].stream),
          "result copy");
     }
-    bool flagged = false;
-    for (auto& s : devs) {
+    bool flagged = false, any_expanded = false;
+    for (std::size_t k = 0; k < devs.size(); ++k) {
+      auto& s = devs[k];
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       ck(cudaStreamSynchronize(s.stream), "hk_eval");
-      if (fgt.on && (halves & hk::kHalfTr) && s.nck > 0) flagged = flagged || *s.h_fgt_flag != 0;
+      if (expanded[k]) flagged = flagged || *s.h_fgt_flag != 0;
+      any_expanded = any_expanded || expanded[k];
     }
-    if (fgt.on && (halves & hk::kHalfTr)) ++fgt_evals;
+    if (any_expanded) ++fgt_evals;
     if (flagged) {
       // a row's certified expansion error could exceed kFgtRowTol: the same
       // evaluation on the direct path (both halves recomputed, caches reset)
       ++fgt_fallbacks;
       for (Key& k : tr_key) k.valid = false;
+      for (Key& k : bg_key) k.valid = false;
       evaluate(p, grad, workspace, /*force=*/true, ll, grad5, single, ell_rows, grad_rows, /*allow_fgt=*/false);
       return;
     }
@@ -1144,9 +1209,13 @@ int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad) {
     const hk::EvalCoef c = ctx->coef(p);
     const hk_ctx::FgtPlan fgt = ctx->fgt_plan(c, with_grad != 0);
     int bgi, tri;
-    const int halves = ctx->plan_halves(c, with_grad != 0, /*force=*/true, bgi, tri, fgt.on);
-    for (auto& s : ctx->devs) ctx->enqueue(s, c, with_grad != 0, halves, bgi, tri, nullptr, nullptr, &fgt);
-    if (fgt.on) {
+    const int halves = ctx->plan_halves(c, with_grad != 0, /*force=*/true, bgi, tri, fgt.on, fgt.bg);
+    bool any = false;
+    for (auto& s : ctx->devs) {
+      s.flag_pending = ctx->enqueue(s, c, with_grad != 0, halves, bgi, tri, nullptr, nullptr, &fgt);
+      any = any || s.flag_pending;
+    }
+    if (any) {
       ++ctx->fgt_evals;
       ctx->fgt_pending = true;
     }
@@ -1235,7 +1304,7 @@ int hk_fgt_stats(hk_ctx* ctx, long* evals, long* fallbacks, int* async_flagged) 
       for (auto& s : ctx->devs) {
         ck(cudaSetDevice(s.dev), "cudaSetDevice");
         ck(cudaStreamSynchronize(s.stream), "hk_fgt_stats");
-        if (s.nck > 0 && *s.h_fgt_flag) flagged = 1;
+        if (s.flag_pending && *s.h_fgt_flag) flagged = 1;
       }
     }
     if (evals) *evals = ctx->fgt_evals;
@@ -1248,6 +1317,7 @@ int hk_set_option(hk_ctx* ctx, int option, int value) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("hk_set_option: null context");
     if (option == HK_OPT_BG_EXPANSION) ctx->bg_expansion = value != 0;
+    else if (option == HK_OPT_BG_FGT) ctx->bg_fgt_enabled = value != 0;
     else if (option == HK_OPT_FGT) ctx->fgt_enabled = value != 0;
     else throw std::invalid_argument("hk_set_option: unknown option " + std::to_string(option));
   });

@@ -109,9 +109,12 @@ __device__ __forceinline__ void fgt_flush(double* ob, int sets, int nb, const do
   }
 }
 
+constexpr int kMomBoxesPerCta = 16;  // grid: (checkpoint, group of 16 boxes)
+
 __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParams F) {
   extern __shared__ __align__(16) double s_dyn[];
   const int k = blockIdx.x;
+  const int B_end = min(F.nbox, (static_cast<int>(blockIdx.y) + 1) * kMomBoxesPerCta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* pu = s_dyn + warp * kMomBatch * (2 * P + 2);
   double* pv = pu + kMomBatch * P;
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParam
   const double tR = F.tR[k];
   const int sets = F.grad ? 2 : 1;
   double* out = F.mom + static_cast<size_t>(k) * F.nbox * 2 * PP;
-  for (int B = warp; B < F.nbox; B += kMomWarps) {
+  for (int B = blockIdx.y * kMomBoxesPerCta + warp; B < B_end; B += kMomWarps) {
     double* ob = out + static_cast<size_t>(B) * 2 * PP;
     for (int c = lane; c < sets * PP; c += 32) ob[c] = 0.0;
     int nb = 0;
@@ -195,7 +198,7 @@ __device__ __forceinline__ void hermite(double s, double (&h)[P + 2]) {
 }
 
 template <bool kGrad>
-__global__ void __launch_bounds__(kFgtEvalThreads, 2)
+__global__ void __launch_bounds__(kFgtEvalThreads, 4)
     fgt_eval_kernel(const FgtParams F, int rows_base, int rows_total, const double* __restrict__ bg_sums,
                     double* __restrict__ tr_sums, double coef_a, double coef_c, unsigned* flag) {
   constexpr int kSets = kGrad ? 2 : 1;
@@ -244,32 +247,42 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 2)
       if (use) w_used += wB;
       else if (valid) w_cut += wB * exp(-d2);
       if (__any_sync(0xffffffffu, use)) {
-        double hx[P + 2], hy[P + 2];
-        hermite<kGrad>(X, hx);
+        // h_b(Y) for every b (register array, static indices); h_a(X) by the
+        // running three-term recurrence inside the a loop (the loop stays
+        // rolled: a fully unrolled P x P body overflows the instruction cache)
+        double hy[P + 2];
         hermite<kGrad>(Y, hy);
+        const double X2 = 2.0 * X;
+        double ha = exp(-X * X), ha1 = X2 * ha;
+        double ha2 = fma(X2, ha1, -2.0 * ha);
         double t0 = 0.0, q1 = 0.0, q2 = 0.0, b0 = 0.0;
-#pragma unroll
+#pragma unroll 2
         for (int a = 0; a < P; ++a) {
+          const double* Ar = A + a * P;
           double sA = 0.0, sA2 = 0.0, sB = 0.0;
 #pragma unroll
           for (int b = 0; b < P; b += 2) {
-            const double2 ab = *reinterpret_cast<const double2*>(A + a * P + b);
+            const double2 ab = *reinterpret_cast<const double2*>(Ar + b);
             sA = fma(ab.x, hy[b], sA);
             sA = fma(ab.y, hy[b + 1], sA);
             if (kGrad) {
               sA2 = fma(ab.x, hy[b + 2], sA2);
               sA2 = fma(ab.y, hy[b + 3], sA2);
-              const double2 bb = *reinterpret_cast<const double2*>(A + PP + a * P + b);
+              const double2 bb = *reinterpret_cast<const double2*>(Ar + PP + b);
               sB = fma(bb.x, hy[b], sB);
               sB = fma(bb.y, hy[b + 1], sB);
             }
           }
-          t0 = fma(hx[a], sA, t0);
+          t0 = fma(ha, sA, t0);
           if (kGrad) {
-            q1 = fma(hx[a + 2], sA, q1);
-            q2 = fma(hx[a], sA2, q2);
-            b0 = fma(hx[a], sB, b0);
+            q1 = fma(ha2, sA, q1);
+            q2 = fma(ha, sA2, q2);
+            b0 = fma(ha, sB, b0);
           }
+          const double ha3 = fma(X2, ha2, -2.0 * (a + 2) * ha1);  // h_{a+3}
+          ha = ha1;
+          ha1 = ha2;
+          ha2 = ha3;
         }
         if (use) {
           T += t0;
@@ -304,6 +317,113 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 2)
   if (!(err <= F.row_tol * S)) atomicOr(flag, 1u);
 }
 
+// ---------------------------------------------------------------------------
+// The background as a 1-D Hermite expansion in time (both variants):
+//   B_i  = sum_{t_j != t_i} exp(-(t_i - t_j)^2 / delta_t),  delta_t = 2 tau^2
+//   B2_i = sum_{t_j != t_i} (t_i - t_j)^2 exp(...)
+// (model.hpp:124-140 and the gradient's B2).  Time boxes of side
+// gamma sqrt(delta_t) are contiguous index ranges of the sorted times; with
+// unit weights A_n = sum_{j in box} u_j^n / n! the full sums over every j are
+//   Bfull_i  = sum_box sum_n A_n h_n(X),
+//   B2full_i = delta_t [ sum_box sum_n A_n h_{n+2}(X) / 4 + Bfull_i / 2 ],
+// and the tied columns (self included) add exactly 1 each to Bfull and 0 to
+// B2full: B_i = Bfull_i - (ub_i - lb_i).  Certification per row: truncation
+// eps per unit weight x the counts of the boxes used, the cut boxes' counts x
+// e^{-d^2}, and the rounding of Bfull against B_i itself (S_i >= a B_i).
+
+constexpr int kBgThreads = 256;
+
+// box ranges (binary search of each box's first time) and moments: one CTA
+// per box; thread-strided partial sums reduced in a fixed tree order
+__global__ void __launch_bounds__(kBgThreads) bg_fgt_moments_kernel(const BgFgtParams F) {
+  __shared__ double s_red[kBgThreads];
+  __shared__ int s_range[2];
+  const int b = blockIdx.x;
+  if (threadIdx.x < 2) {
+    const int box = b + threadIdx.x;  // first index whose box >= `box`
+    int lo = 0, hi = F.n;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const int bx = min(max(static_cast<int>(floor((F.t[mid] - F.t0) / F.L)), 0), F.nbt - 1);
+      if (bx < box) lo = mid + 1;
+      else hi = mid;
+    }
+    s_range[threadIdx.x] = box >= F.nbt ? F.n : lo;
+  }
+  __syncthreads();
+  const int j0 = s_range[0], j1 = s_range[1];
+  const double c = F.t0 + (b + 0.5) * F.L;
+  double acc[P];
+#pragma unroll
+  for (int n = 0; n < P; ++n) acc[n] = 0.0;
+  for (int j = j0 + threadIdx.x; j < j1; j += kBgThreads) {
+    const double u = (F.t[j] - c) * F.inv_sqd;
+    double pw = 1.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+      acc[n] += pw;
+      pw = pw * u / (n + 1);
+    }
+  }
+  for (int n = 0; n < P; ++n) {
+    s_red[threadIdx.x] = acc[n];
+    __syncthreads();
+    for (int h = kBgThreads / 2; h > 0; h >>= 1) {
+      if (threadIdx.x < h) s_red[threadIdx.x] += s_red[threadIdx.x + h];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) F.mom[b * P + n] = s_red[0];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) F.count[b] = j1 - j0;
+}
+
+__global__ void __launch_bounds__(kBgThreads) bg_fgt_eval_kernel(const BgFgtParams F, int rows_base,
+                                                                  int rows_total, double* bg_sums,
+                                                                  unsigned* flag) {
+  const int li = blockIdx.x * kBgThreads + threadIdx.x;
+  if (li >= rows_total) return;
+  const int row = rows_base + li;
+  const double ti = F.t[row];
+  const double reach = sqrt(kFgtCut) / F.inv_sqd + 0.5 * F.L;  // box centres farther: cut
+  const int b0 = max(0, static_cast<int>(floor((ti - reach - F.t0) / F.L)));
+  const int b1 = min(F.nbt - 1, static_cast<int>(floor((ti + reach - F.t0) / F.L)));
+  const double hs = 0.5 * F.L * F.inv_sqd;
+  // every box outside [b0, b1] is farther than sqrt(kFgtCut) scaled units:
+  // its columns add at most e^{-kFgtCut} each (the `cut` bound below)
+  double Bf = 0.0, Q = 0.0, used = 0.0;
+  for (int b = b0; b <= b1; ++b) {
+    const double X = (ti - (F.t0 + (b + 0.5) * F.L)) * F.inv_sqd;
+    const double d = fmax(fabs(X) - hs, 0.0);
+    if (d * d > kFgtCut) continue;
+    used += F.count[b];
+    const double* A = F.mom + b * P;
+    const double X2 = 2.0 * X;
+    double h0 = exp(-X * X), h1 = X2 * h0;
+    double h2 = fma(X2, h1, -2.0 * h0);
+    double s0 = 0.0, s2 = 0.0;
+#pragma unroll
+    for (int n = 0; n < P; ++n) {
+      s0 = fma(A[n], h0, s0);
+      s2 = fma(A[n], h2, s2);
+      const double h3 = fma(X2, h2, -2.0 * (n + 2) * h1);
+      h0 = h1;
+      h1 = h2;
+      h2 = h3;
+    }
+    Bf += s0;
+    Q += s2;
+  }
+  const double ties = static_cast<double>(F.ub[row] - F.lb[row]);
+  const double B = Bf - ties;
+  const double B2 = F.delta * fma(0.25, Q, 0.5 * Bf);
+  bg_sums[li] = B;
+  bg_sums[rows_total + li] = B2;
+  const double cut = (F.n - used) * exp(-kFgtCut);
+  const double err = F.eps * used + cut + 2.3e-16 * (Bf + ties);
+  if (!(err <= F.row_tol * B)) atomicOr(flag, 1u);
+}
+
 }  // namespace
 
 double fgt_truncation_bound(int p, double gamma) {
@@ -323,8 +443,24 @@ void launch_fgt_prepare(const FgtParams& F, cudaStream_t s) {
   fgt_refs_kernel<<<(F.nck + 127) / 128, 128, 0, s>>>(F);
   if (F.ncols > 0) fgt_assign_kernel<<<(F.ncols + 255) / 256, 256, 0, s>>>(F);
   cudaFuncSetAttribute(fgt_moments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMomSmem);
-  fgt_moments_kernel<<<F.nck, kMomThreads, kMomSmem, s>>>(F);
+  const dim3 grid(F.nck, (F.nbox + kMomBoxesPerCta - 1) / kMomBoxesPerCta);
+  fgt_moments_kernel<<<grid, kMomThreads, kMomSmem, s>>>(F);
   fgt_scan_kernel<<<(F.nbox * PP + 255) / 256, 256, 0, s>>>(F);
+}
+
+double bg_fgt_truncation_bound(int p, double gamma) {
+  const double K = 1.0865;
+  const double rho = gamma / std::sqrt(2.0);
+  double tail = 1.0;  // rho^p / sqrt(p!)
+  for (int n = 1; n <= p; ++n) tail *= rho / std::sqrt(static_cast<double>(n));
+  return K * tail / (1.0 - rho / std::sqrt(p + 1.0));
+}
+
+void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* bg_sums, unsigned* flag,
+                   cudaStream_t s) {
+  bg_fgt_moments_kernel<<<F.nbt, kBgThreads, 0, s>>>(F);
+  bg_fgt_eval_kernel<<<(rows_total + kBgThreads - 1) / kBgThreads, kBgThreads, 0, s>>>(F, rows_base, rows_total,
+                                                                                     bg_sums, flag);
 }
 
 void launch_fgt_eval(const FgtParams& F, int rows_base, int rows_total, const double* bg_sums,

@@ -33,6 +33,24 @@ struct FgtParams {
   double* mom;                  // [nck][nbox][2][kFgtP^2]: A (and B) moments
 };
 
+// The background's 1-D expansion in time (hk_fgt.cu, both variants).
+constexpr int kBgFgtMaxBoxes = 1 << 16;
+struct BgFgtParams {
+  int n;                        // catalog size
+  const double* t;              // sorted times
+  const int *lb, *ub;           // tie bounds (count_before / upper_bound)
+  int nbt;                      // time boxes
+  double t0, L, inv_sqd;        // first time, box side gamma sqrt(2 tau^2), 1/sqrt(2 tau^2)
+  double delta;                 // 2 tau^2
+  double eps, row_tol;          // truncation bound per unit weight; certified relative bound
+  double* mom;                  // [nbt][kFgtP] moments
+  int* count;                   // [nbt] columns per box
+};
+double bg_fgt_truncation_bound(int p, double gamma);
+// moments + the rows [rows_base, rows_base + rows_total): bg_sums planes B, B2.
+void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* bg_sums, unsigned* flag,
+                   cudaStream_t s);
+
 // eps_p of hk_fgt.cu for p terms and box side gamma sqrt(delta).
 double fgt_truncation_bound(int p, double gamma);
 // reference times, box assignment, increment moments and their scan.

@@ -293,6 +293,10 @@ class Evaluator:
         """HK_OPT_FGT: the homogeneous trigger's Hermite expansion (default on)."""
         check(lib.hk_set_option(self._h, _lib.HK_OPT_FGT, int(on)))
 
+    def set_bg_fgt(self, on: bool) -> None:
+        """HK_OPT_BG_FGT: the background's 1-D Hermite expansion in time (default on)."""
+        check(lib.hk_set_option(self._h, _lib.HK_OPT_BG_FGT, int(on)))
+
     def fgt_stats(self):
         """(evaluations through the expansion, direct recomputations, last
         async evaluation flagged)."""

@@ -1,6 +1,7 @@
-"""The homogeneous trigger's certified Hermite expansion (hk_fgt.cu,
-DESIGN.md section 3b) against the direct per-pair path of the same engine
-(HK_OPT_FGT off) and against the oracle: LL within 1e-13 relative, every
+"""The certified Hermite expansions (hk_fgt.cu): the
+homogeneous trigger's 2-D expansion (HK_OPT_FGT) and the background's 1-D
+expansion in time (HK_OPT_BG_FGT), against the direct per-pair path of the
+same engine and against the oracle: LL within 1e-13 relative, every
 gradient component within 1e-12 of the conditioning scale; the expansion is
 really used (hk_fgt_stats), a failed certification recomputes directly, and
 cached workspace results stay bitwise equal to fresh ones."""
@@ -118,6 +119,7 @@ def test_fgt_certification_fallback(eng, monkeypatch):
     p = eng.HawkesParams(**BENCH)
     direct = eng.Evaluator(cat)
     direct.set_fgt(False)
+    direct.set_bg_fgt(False)  # the fallback recomputes without either expansion
     want = direct.eval(p, grad=True)
     monkeypatch.setenv("HK_FGT_ROW_TOL", "0")
     ev = eng.Evaluator(cat)
@@ -155,3 +157,57 @@ def test_fgt_subquadratic(eng):
     ms_d, _, _ = ev.profile()
     print(f"N=4e5 LL+grad pair+expansion time: expansion {ms_f:.1f} ms, direct {ms_d:.1f} ms")
     assert ms_f < 0.5 * ms_d
+
+
+def direct_ev(eng, cat):
+    ev = eng.Evaluator(cat)
+    ev.set_fgt(False)
+    ev.set_bg_fgt(False)
+    return ev
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_bg_fgt_matches_direct(eng, variant):
+    """The background's 1-D expansion against the pair kernels' background
+    (block expansion and per-pair), both variants, LL + gradient."""
+    cat = eng.benchmark_catalog(200000, 42)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant(variant))
+    ev = eng.Evaluator(cat)
+    ev.set_fgt(False)
+    e0 = ev.fgt_stats()[0]
+    a = ev.eval(p, grad=True)
+    assert ev.fgt_stats()[0] == e0 + 1 and ev.fgt_stats()[1] == 0
+    b = direct_ev(eng, cat).eval(p, grad=True)
+    close(a, b)
+
+
+@pytest.mark.parametrize("tau", [0.02, 0.7, 60.0])
+def test_bg_fgt_tau_range_and_ties(eng, tau):
+    """Short and long background lengthscales (thousands of time boxes / a
+    single box) on a catalog with heavy time ties (ties: exactly 1 each is
+    removed from the full sum)."""
+    rng = np.random.default_rng(17)
+    n = 60000
+    t = np.sort(np.round(rng.uniform(0, 100, n) * 7) / 7)
+    cat = eng.Catalog(t, rng.uniform(-5, 5, n), rng.uniform(-5, 5, n), rng.uniform(1, 100, n))
+    for v in (0, 1):
+        p = eng.HawkesParams(**dict(BENCH, tau_t=tau), variant=eng.Variant(v))
+        a = eng.Evaluator(cat).eval(p, grad=True)
+        b = direct_ev(eng, cat).eval(p, grad=True)
+        close(a, b)
+
+
+def test_bg_fgt_certification_on_sparse_catalogs(eng, oracle):
+    """Catalogs whose background sums are tiny next to their tied/self terms
+    (one event; events 10 lengthscales apart; every row clipped): the
+    certification fails and the evaluation is recomputed directly, exact
+    against the oracle."""
+    p1 = dict(mu0=1.0, tau_t=1.0, xi0=1.0, sigma_x=1.0, sigma_t=1.0, area=1.0)
+    for cat in (eng.Catalog([0.0], [0.0], [0.0]),
+                eng.Catalog(np.arange(3000) * 10.0, np.zeros(3000), np.zeros(3000))):
+        ev = eng.Evaluator(cat)
+        ll, g = ev.eval(eng.HawkesParams(**p1), grad=True)
+        ref = direct_ev(eng, cat).eval(eng.HawkesParams(**p1), grad=True)
+        assert ll == ref[0] and np.array_equal(g, ref[1])
+        assert ev.fgt_stats()[1] == 1  # recomputed on the direct path
+        assert ll == pytest.approx(oracle.ll_grad(cat.arrays(), p1, 0)[0], rel=1e-12)

@@ -333,6 +333,7 @@ def test_bg_expansion_matches_direct(eng, variant):
     cat = eng.benchmark_catalog(100000, 42)
     p = hp(eng, BENCH, variant)
     ev = eng.Evaluator(cat)
+    ev.set_bg_fgt(False)  # the background in the pair kernels (not the 1-D Hermite expansion)
     ll_x, g_x = ev.eval(p, grad=True)
     ev.set_bg_expansion(False)
     ll_d, g_d = ev.eval(p, grad=True)
