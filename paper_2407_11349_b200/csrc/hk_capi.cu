@@ -172,7 +172,7 @@ struct DeviceState {
   int nck = 0, fgt_cols = 0;
   double fgt_direct_cost = 0.0;  // trigger pairs the expansion replaces (sum over rows of P_k)
   int* ck_P = nullptr;                                   // [nck]
-  double *fgt_tR = nullptr, *fgt_decay = nullptr, *fgt_dt = nullptr;  // [nck]
+  double *fgt_tR = nullptr, *fgt_decay = nullptr, *fgt_dt = nullptr, *fgt_wsum = nullptr;  // [nck]
   int* fgt_box = nullptr;                                // [fgt_cols]
   double *fgt_u = nullptr, *fgt_v = nullptr;             // [fgt_cols]
   double* fgt_mom = nullptr;                             // [nck][nbox][2][P^2], grown on demand
@@ -279,7 +279,7 @@ struct hk_ctx {
       for (void* q : {static_cast<void*>(s.ck_P), static_cast<void*>(s.fgt_tR), static_cast<void*>(s.fgt_decay),
                       static_cast<void*>(s.fgt_dt), static_cast<void*>(s.fgt_box), static_cast<void*>(s.fgt_u),
                       static_cast<void*>(s.fgt_v), static_cast<void*>(s.fgt_mom), static_cast<void*>(s.fgt_flag),
-                      static_cast<void*>(s.bgf_mom), static_cast<void*>(s.bgf_count)})
+                      static_cast<void*>(s.bgf_mom), static_cast<void*>(s.bgf_count), static_cast<void*>(s.fgt_wsum)})
         if (q) cudaFree(q);
       if (s.h_fgt_flag) cudaFreeHost(s.h_fgt_flag);
       if (s.gather6) cudaFree(s.gather6);
@@ -470,6 +470,7 @@ struct hk_ctx {
       s.fgt_tR = dmalloc<double>(s.nck);
       s.fgt_decay = dmalloc<double>(s.nck);
       s.fgt_dt = dmalloc<double>(s.nck);
+      s.fgt_wsum = dmalloc<double>(s.nck);
       s.fgt_box = dmalloc<int>(s.fgt_cols);
       s.fgt_u = dmalloc<double>(s.fgt_cols);
       s.fgt_v = dmalloc<double>(s.fgt_cols);
@@ -623,6 +624,7 @@ struct hk_ctx {
     F.u = s.fgt_u;
     F.v = s.fgt_v;
     F.mom = s.fgt_mom;
+    F.wsum = s.fgt_wsum;
     return F;
   }
 

@@ -55,6 +55,18 @@ namespace {
 constexpr int P = kFgtP;
 constexpr int PP = kFgtP * kFgtP;
 
+// 1 / (n + 1), n < P: the power tables u^n / n! by multiplications (an FP64
+// division is a long instruction sequence on the GPU)
+struct Recip {
+  double v[P];
+};
+constexpr Recip make_recip() {
+  Recip r{};
+  for (int n = 0; n < P; ++n) r.v[n] = 1.0 / (n + 1);
+  return r;
+}
+__constant__ Recip c_recip = make_recip();
+
 // ---------------------------------------------------------------------------
 // per checkpoint: reference time, decay from the previous one
 
@@ -95,17 +107,34 @@ __global__ void fgt_assign_kernel(const FgtParams F) {
 constexpr int kMomThreads = 128;
 constexpr int kMomWarps = kMomThreads / 32;
 constexpr int kMomBatch = 32;  // sources per batch and warp (one 32-column chunk fits)
-// dynamic shared memory: per warp kMomBatch x (P + P + 2) doubles
-constexpr int kMomSmem = kMomWarps * kMomBatch * (2 * P + 2) * static_cast<int>(sizeof(double));
+// dynamic shared memory: per warp kMomBatch x 3P doubles (W u^a/a!, (t_R - t) W u^a/a!, v^b/b!)
+constexpr int kMomSmem = kMomWarps * kMomBatch * (3 * P) * static_cast<int>(sizeof(double));
 
-// adds the batch's sources (in batch order) to the box's coefficients
-__device__ __forceinline__ void fgt_flush(double* ob, int sets, int nb, const double* pu, const double* pv,
-                                          const double* w, int lane) {
-  for (int c = lane; c < sets * PP; c += 32) {
-    const int set = c / PP, a = (c % PP) / P, b = c % P;
-    double acc = ob[c];
-    for (int s = 0; s < nb; ++s) acc = fma(w[2 * s + set] * pu[s * P + a], pv[s * P + b], acc);
-    ob[c] = acc;
+// adds the batch's sources (in batch order) to the box's coefficients: lane
+// b (< P) owns the coefficients (a, b) of both sets for every a, so per
+// source it reads its v^b/b! once and the broadcast u^a/a! weights
+__device__ __forceinline__ void fgt_flush(double* ob, bool grad, int nb, const double* wpu, const double* pv,
+                                          int lane) {
+  if (lane >= P) return;
+  double accA[P], accB[P];
+#pragma unroll
+  for (int a = 0; a < P; ++a) {
+    accA[a] = ob[a * P + lane];
+    accB[a] = grad ? ob[PP + a * P + lane] : 0.0;
+  }
+  for (int s = 0; s < nb; ++s) {
+    const double vb = pv[s * P + lane];
+    const double* wa = wpu + s * 2 * P;  // [W u^a / a!, (t_R - t) W u^a / a!]
+#pragma unroll
+    for (int a = 0; a < P; ++a) {
+      accA[a] = fma(wa[a], vb, accA[a]);
+      if (grad) accB[a] = fma(wa[P + a], vb, accB[a]);
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < P; ++a) {
+    ob[a * P + lane] = accA[a];
+    if (grad) ob[PP + a * P + lane] = accB[a];
   }
 }
 
@@ -116,16 +145,16 @@ __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParam
   const int k = blockIdx.x;
   const int B_end = min(F.nbox, (static_cast<int>(blockIdx.y) + 1) * kMomBoxesPerCta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* pu = s_dyn + warp * kMomBatch * (2 * P + 2);
-  double* pv = pu + kMomBatch * P;
-  double* w = pv + kMomBatch * P;
+  double* wpu = s_dyn + warp * kMomBatch * (3 * P);  // [s][2][P]
+  double* pv = wpu + kMomBatch * 2 * P;              // [s][P]
   const int j0 = k ? F.P[k - 1] : 0, j1 = F.P[k];
   const double tR = F.tR[k];
-  const int sets = F.grad ? 2 : 1;
+  const bool grad = F.grad != 0;
   double* out = F.mom + static_cast<size_t>(k) * F.nbox * 2 * PP;
   for (int B = blockIdx.y * kMomBoxesPerCta + warp; B < B_end; B += kMomWarps) {
     double* ob = out + static_cast<size_t>(B) * 2 * PP;
-    for (int c = lane; c < sets * PP; c += 32) ob[c] = 0.0;
+    for (int c = lane; c < (grad ? 2 : 1) * PP; c += 32) ob[c] = 0.0;
+    __syncwarp();
     int nb = 0;
     for (int c0 = j0; c0 < j1; c0 += 32) {
       const int j = c0 + lane;
@@ -135,29 +164,31 @@ __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParam
       if (cnt == 0) continue;
       if (nb + cnt > kMomBatch) {
         __syncwarp();
-        fgt_flush(ob, sets, nb, pu, pv, w, lane);
+        fgt_flush(ob, grad, nb, wpu, pv, lane);
         __syncwarp();
         nb = 0;
       }
       if (in) {
         const int s = nb + __popc(m & ((1u << lane) - 1u));
         const double u = F.u[j], v = F.v[j];
-        const double wj = exp(-F.omega * (tR - F.t[j]));
-        w[2 * s] = wj;
-        w[2 * s + 1] = (tR - F.t[j]) * wj;
-        double a1 = 1.0, b1 = 1.0;
+        const double dtj = tR - F.t[j];
+        const double wj = exp(-F.omega * dtj);
+        double a1 = wj, a2 = dtj * wj, b1 = 1.0;
 #pragma unroll 1
         for (int n = 0; n < P; ++n) {
-          pu[s * P + n] = a1;
+          wpu[s * 2 * P + n] = a1;
+          wpu[s * 2 * P + P + n] = a2;
           pv[s * P + n] = b1;
-          a1 = a1 * u / (n + 1);
-          b1 = b1 * v / (n + 1);
+          const double f = c_recip.v[n];
+          a1 = a1 * u * f;
+          a2 = a2 * u * f;
+          b1 = b1 * v * f;
         }
       }
       nb += cnt;
     }
     __syncwarp();
-    if (nb) fgt_flush(ob, sets, nb, pu, pv, w, lane);
+    if (nb) fgt_flush(ob, grad, nb, wpu, pv, lane);
     __syncwarp();
   }
 }
@@ -169,6 +200,7 @@ __global__ void fgt_scan_kernel(const FgtParams F) {
   if (c >= F.nbox * PP) return;
   const int B = c / PP, ab = c % PP;
   double ma = 0.0, mb = 0.0;
+#pragma unroll 4
   for (int k = 0; k < F.nck; ++k) {
     double* m = F.mom + (static_cast<size_t>(k) * F.nbox + B) * 2 * PP + ab;
     const double d = F.decay[k], dt = F.dt[k];
@@ -197,20 +229,34 @@ __device__ __forceinline__ void hermite(double s, double (&h)[P + 2]) {
   for (int n = 1; n < P + 1; ++n) h[n + 1] = fma(2.0 * s, h[n], -2.0 * n * h[n - 1]);
 }
 
+// kFgtRowsPerThread rows per thread (rows li and li + kFgtEvalThreads of the
+// CTA's 2 x kFgtEvalThreads rows): every moment pair read from shared memory
+// feeds both rows' multiply-adds (half the loads per FMA, twice the
+// independent accumulation chains per warp).
 template <bool kGrad>
-__global__ void __launch_bounds__(kFgtEvalThreads, 4)
+__global__ void __launch_bounds__(kFgtEvalThreads, 2)
     fgt_eval_kernel(const FgtParams F, int rows_base, int rows_total, const double* __restrict__ bg_sums,
                     double* __restrict__ tr_sums, double coef_a, double coef_c, unsigned* flag) {
+  constexpr int R = kFgtRowsPerThread;
   constexpr int kSets = kGrad ? 2 : 1;
   constexpr unsigned kBoxBytes = kSets * PP * sizeof(double);
   __shared__ __align__(128) double s_m[2][kSets * PP];
   __shared__ __align__(8) uint64_t s_bar[2];
-  const int li = blockIdx.x * kFgtEvalThreads + threadIdx.x;
-  const int row_block = (blockIdx.x * kFgtEvalThreads) / kFgtRowBlock;
+  const int cta_rows = R * kFgtEvalThreads;
+  const int row_block = (blockIdx.x * cta_rows) / kFgtRowBlock;
   const int k = row_block / kFgtBlocks;
-  const bool valid = li < rows_total;
-  const int row = rows_base + (valid ? li : rows_total - 1);
-  const double xi = F.x[row], yi = F.y[row], ti = F.t[row];
+  int li[R];
+  bool valid[R];
+  double xi[R], yi[R], ti[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    li[r] = blockIdx.x * cta_rows + r * kFgtEvalThreads + threadIdx.x;
+    valid[r] = li[r] < rows_total;
+    const int row = rows_base + (valid[r] ? li[r] : rows_total - 1);
+    xi[r] = F.x[row];
+    yi[r] = F.y[row];
+    ti[r] = F.t[row];
+  }
   const double* mk = F.mom + static_cast<size_t>(k) * F.nbox * 2 * PP;
   if (threadIdx.x == 0) {
     mbar_init(&s_bar[0], 1);
@@ -219,8 +265,9 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 4)
   }
   __syncthreads();
   const bool any = F.P[k] > 0;  // checkpoint with no earlier columns: nothing to add
-  double T = 0.0, Td = 0.0, Tq = 0.0, Tq2 = 0.0;
-  double w_used = 0.0, w_cut = 0.0;  // box weights (A_00 = sum W) used / skipped with their bound
+  double T[R], Td[R], Tq[R], Tq2[R], w_used[R];  // w_used: box weights (A_00 = sum W) evaluated
+#pragma unroll
+  for (int r = 0; r < R; ++r) T[r] = Td[r] = Tq[r] = Tq2[r] = w_used[r] = 0.0;
   const double hs = 0.5 * F.L * F.inv_sqd;  // half box side, scaled
   if (any) {
     if (threadIdx.x == 0) {
@@ -238,83 +285,121 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 4)
       phases ^= 1u << st;
       const double* A = s_m[st];
       const int bx = B % F.nb, by = B / F.nb;
-      const double X = (xi - (F.x0 + (bx + 0.5) * F.L)) * F.inv_sqd;
-      const double Y = (yi - (F.y0 + (by + 0.5) * F.L)) * F.inv_sqd;
-      const double dx = fmax(fabs(X) - hs, 0.0), dy = fmax(fabs(Y) - hs, 0.0);
-      const double d2 = fma(dx, dx, dy * dy);
-      const bool use = valid && d2 <= kFgtCut;
-      const double wB = A[0];  // sum of the box's weights (>= 0)
-      if (use) w_used += wB;
-      else if (valid) w_cut += wB * exp(-d2);
-      if (__any_sync(0xffffffffu, use)) {
-        // h_b(Y) for every b (register array, static indices); h_a(X) by the
+      const double cxB = F.x0 + (bx + 0.5) * F.L, cyB = F.y0 + (by + 0.5) * F.L;
+      double X[R], Y[R];
+      bool use[R], any_use = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        X[r] = (xi[r] - cxB) * F.inv_sqd;
+        Y[r] = (yi[r] - cyB) * F.inv_sqd;
+        const double dx = fmax(fabs(X[r]) - hs, 0.0), dy = fmax(fabs(Y[r]) - hs, 0.0);
+        use[r] = valid[r] && fma(dx, dx, dy * dy) <= kFgtCut;
+        if (use[r]) w_used[r] += A[0];  // sum of the box's weights (>= 0)
+        any_use = any_use || use[r];
+      }
+      if (__any_sync(0xffffffffu, any_use)) {
+        // h_b(Y) for every b (register arrays, static indices); h_a(X) by the
         // running three-term recurrence inside the a loop (the loop stays
         // rolled: a fully unrolled P x P body overflows the instruction cache)
-        double hy[P + 2];
-        hermite<kGrad>(Y, hy);
-        const double X2 = 2.0 * X;
-        double ha = exp(-X * X), ha1 = X2 * ha;
-        double ha2 = fma(X2, ha1, -2.0 * ha);
-        double t0 = 0.0, q1 = 0.0, q2 = 0.0, b0 = 0.0;
-#pragma unroll 2
+        double hy[R][P + 2];
+        double X2[R], ha[R], ha1[R], ha2[R];
+        double t0[R], q1[R], q2[R], b0[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          hermite<kGrad>(Y[r], hy[r]);
+          X2[r] = 2.0 * X[r];
+          ha[r] = exp(-X[r] * X[r]);
+          ha1[r] = X2[r] * ha[r];
+          ha2[r] = fma(X2[r], ha1[r], -2.0 * ha[r]);
+          t0[r] = q1[r] = q2[r] = b0[r] = 0.0;
+        }
+#pragma unroll 1
         for (int a = 0; a < P; ++a) {
           const double* Ar = A + a * P;
-          double sA = 0.0, sA2 = 0.0, sB = 0.0;
+          double sA[R], sA2[R], sB[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) sA[r] = sA2[r] = sB[r] = 0.0;
 #pragma unroll
           for (int b = 0; b < P; b += 2) {
             const double2 ab = *reinterpret_cast<const double2*>(Ar + b);
-            sA = fma(ab.x, hy[b], sA);
-            sA = fma(ab.y, hy[b + 1], sA);
-            if (kGrad) {
-              sA2 = fma(ab.x, hy[b + 2], sA2);
-              sA2 = fma(ab.y, hy[b + 3], sA2);
-              const double2 bb = *reinterpret_cast<const double2*>(Ar + PP + b);
-              sB = fma(bb.x, hy[b], sB);
-              sB = fma(bb.y, hy[b + 1], sB);
+            double2 bb;
+            if (kGrad) bb = *reinterpret_cast<const double2*>(Ar + PP + b);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              sA[r] = fma(ab.x, hy[r][b], sA[r]);
+              sA[r] = fma(ab.y, hy[r][b + 1], sA[r]);
+              if (kGrad) {
+                sA2[r] = fma(ab.x, hy[r][b + 2], sA2[r]);
+                sA2[r] = fma(ab.y, hy[r][b + 3], sA2[r]);
+                sB[r] = fma(bb.x, hy[r][b], sB[r]);
+                sB[r] = fma(bb.y, hy[r][b + 1], sB[r]);
+              }
             }
           }
-          t0 = fma(ha, sA, t0);
-          if (kGrad) {
-            q1 = fma(ha2, sA, q1);
-            q2 = fma(ha, sA2, q2);
-            b0 = fma(ha, sB, b0);
-          }
-          const double ha3 = fma(X2, ha2, -2.0 * (a + 2) * ha1);  // h_{a+3}
-          ha = ha1;
-          ha1 = ha2;
-          ha2 = ha3;
-        }
-        if (use) {
-          T += t0;
-          if (kGrad) {
-            Td += b0;
-            Tq += q1;
-            Tq2 += q2;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            t0[r] = fma(ha[r], sA[r], t0[r]);
+            if (kGrad) {
+              q1[r] = fma(ha2[r], sA[r], q1[r]);
+              q2[r] = fma(ha[r], sA2[r], q2[r]);
+              b0[r] = fma(ha[r], sB[r], b0[r]);
+            }
+            const double ha3 = fma(X2[r], ha2[r], -2.0 * (a + 2) * ha1[r]);  // h_{a+3}
+            ha[r] = ha1[r];
+            ha1[r] = ha2[r];
+            ha2[r] = ha3;
           }
         }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (use[r]) {
+            T[r] += t0[r];
+            if (kGrad) {
+              Td[r] += b0[r];
+              Tq[r] += q1[r];
+              Tq2[r] += q2[r];
+            }
+          }
       }
       __syncthreads();  // every warp is done with this stage before it is refilled
     }
   }
-  if (!valid || !any) return;
+  if (!any) return;
   const double tR = F.tR[k];
-  const double E = exp(-F.omega * (ti - tR));
   double* trT = tr_sums;
   double* trTd = tr_sums + rows_total;
   double* trTq = tr_sums + 2 * static_cast<size_t>(rows_total);
-  const double addT = E * T;
-  const double Ttot = trT[li] + addT;
-  trT[li] = Ttot;
-  if (kGrad) {
-    trTd[li] += E * fma(ti - tR, T, Td);
-    trTq[li] += E * F.delta * fma(0.25, Tq + Tq2, T);
+  // the boxes not evaluated are farther than sqrt(kFgtCut) scaled units:
+  // their total weight (the prefix's, sum_B A_00, minus the evaluated boxes')
+  // contributes at most e^{-kFgtCut} per unit
+  const double w_all = F.wsum[k];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (!valid[r]) continue;
+    const double E = exp(-F.omega * (ti[r] - tR));
+    const double Ttot = trT[li[r]] + E * T[r];
+    trT[li[r]] = Ttot;
+    if (kGrad) {
+      trTd[li[r]] += E * fma(ti[r] - tR, T[r], Td[r]);
+      trTq[li[r]] += E * F.delta * fma(0.25, Tq[r] + Tq2[r], T[r]);
+    }
+    // certification: what the expansion may have dropped (truncation per
+    // unit weight of the boxes used, the cut boxes' weight bound) against
+    // the row's rate S_i = a B_i + c T_i (gradient terms: same weights, the
+    // h_{n+2} terms inflate the truncation bound by at most 2 (p + 1))
+    const double err = coef_c * E * (F.eps * w_used[r] + fmax(w_all - w_used[r], 0.0) * exp(-kFgtCut));
+    const double S = coef_a * bg_sums[li[r]] + coef_c * Ttot;
+    if (!(err <= F.row_tol * S)) atomicOr(flag, 1u);
   }
-  // certification: the bound on what the expansion may have dropped, against
-  // the row's rate S_i = a B_i + c T_i (gradient terms: same weights, the
-  // h_{n+2} terms inflate the truncation bound by F.eps_grad / F.eps)
-  const double err = coef_c * E * (F.eps * w_used + w_cut);
-  const double S = coef_a * bg_sums[li] + coef_c * Ttot;
-  if (!(err <= F.row_tol * S)) atomicOr(flag, 1u);
+}
+
+// the total weight of each checkpoint's prefix (sum over boxes of A_00)
+__global__ void fgt_wsum_kernel(const FgtParams F) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= F.nck) return;
+  double w = 0.0;
+  for (int B = 0; B < F.nbox; ++B) w += F.mom[(static_cast<size_t>(k) * F.nbox + B) * 2 * PP];
+  F.wsum[k] = w;
 }
 
 // ---------------------------------------------------------------------------
@@ -362,9 +447,10 @@ __global__ void __launch_bounds__(kBgThreads) bg_fgt_moments_kernel(const BgFgtP
 #pragma unroll
     for (int n = 0; n < P; ++n) {
       acc[n] += pw;
-      pw = pw * u / (n + 1);
+      pw = pw * u * c_recip.v[n];
     }
   }
+#pragma unroll
   for (int n = 0; n < P; ++n) {
     s_red[threadIdx.x] = acc[n];
     __syncthreads();
@@ -446,6 +532,7 @@ void launch_fgt_prepare(const FgtParams& F, cudaStream_t s) {
   const dim3 grid(F.nck, (F.nbox + kMomBoxesPerCta - 1) / kMomBoxesPerCta);
   fgt_moments_kernel<<<grid, kMomThreads, kMomSmem, s>>>(F);
   fgt_scan_kernel<<<(F.nbox * PP + 255) / 256, 256, 0, s>>>(F);
+  fgt_wsum_kernel<<<(F.nck + 127) / 128, 128, 0, s>>>(F);
 }
 
 double bg_fgt_truncation_bound(int p, double gamma) {
@@ -465,7 +552,8 @@ void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* 
 
 void launch_fgt_eval(const FgtParams& F, int rows_base, int rows_total, const double* bg_sums,
                      double* tr_sums, double coef_a, double coef_c, unsigned* flag, cudaStream_t s) {
-  const int blocks = (rows_total + kFgtEvalThreads - 1) / kFgtEvalThreads;
+  const int rows_per_cta = kFgtRowsPerThread * kFgtEvalThreads;
+  const int blocks = (rows_total + rows_per_cta - 1) / rows_per_cta;
   if (F.grad)
     fgt_eval_kernel<true><<<blocks, kFgtEvalThreads, 0, s>>>(F, rows_base, rows_total, bg_sums, tr_sums,
                                                              coef_a, coef_c, flag);

@@ -9,7 +9,8 @@ constexpr int kFgtP = 30;              // Hermite terms per dimension (a, b < kF
 constexpr double kFgtGamma = 1.4142135623730951;  // box side / sqrt(delta): rho = 1
 constexpr int kFgtBlocks = 4;          // homogeneous row blocks per checkpoint
 constexpr int kFgtRowBlock = 512;      // rows per block of the homogeneous plan (rows_per_item(false))
-constexpr int kFgtEvalThreads = 128;   // rows per evaluation CTA (divides kFgtRowBlock)
+constexpr int kFgtEvalThreads = 128;   // threads per evaluation CTA
+constexpr int kFgtRowsPerThread = 2;   // rows per thread (kFgtEvalThreads x this divides kFgtRowBlock)
 constexpr double kFgtCut = 46.0;       // boxes farther than sqrt(46) scaled units are skipped
 constexpr double kFgtRowTol = 1e-13;   // certified per-row relative error bound, else recompute directly
 constexpr int kFgtMaxBoxes = 1024;     // larger grids (small sigma_x / wide catalogs): direct path
@@ -31,6 +32,7 @@ struct FgtParams {
   int* box;                     // [ncols]
   double *u, *v;                // [ncols] scaled offsets from the box centre
   double* mom;                  // [nck][nbox][2][kFgtP^2]: A (and B) moments
+  double* wsum;                 // [nck] total prefix weight (sum over boxes of A_00)
 };
 
 // The background's 1-D expansion in time (hk_fgt.cu, both variants).

@@ -61,18 +61,18 @@ struct Philox {
 struct Uniforms {
   uint2 key;
   unsigned event, ctr_lo, ctr_hi, draw = 0;
-  double buf[2];
+  double u0 = 0.0, u1 = 0.0;
   int left = 0;
   __device__ double next() {
     if (left == 0) {
       const uint4 r = Philox::gen(make_uint4(event, ctr_lo, ctr_hi, draw++), key);
       const unsigned long long a = (static_cast<unsigned long long>(r.x) << 32 | r.y) >> 11;
       const unsigned long long b = (static_cast<unsigned long long>(r.z) << 32 | r.w) >> 11;
-      buf[0] = static_cast<double>(a) * 0x1.0p-53;
-      buf[1] = static_cast<double>(b) * 0x1.0p-53;
+      u0 = static_cast<double>(a) * 0x1.0p-53;
+      u1 = static_cast<double>(b) * 0x1.0p-53;
       left = 2;
     }
-    return buf[2 - left--];
+    return left-- == 2 ? u0 : u1;
   }
 };
 
