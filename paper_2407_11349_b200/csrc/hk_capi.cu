@@ -325,6 +325,10 @@ struct hk_ctx {
     set_bbox(xmin, xmax, ymin, ymax, n);
   }
 
+  // The multi-device data plane is active (several devices, or one forced
+  // through NCCL).
+  bool multi() const { return devs.size() > 1 || use_nccl; }
+
   // Multi-device set-up after every device is initialised: NCCL
   // communicators over distinct devices (HK_NO_NCCL=1 or a repeated device:
   // peer copies), the gather buffers, and device 0's bbox buffers.
@@ -334,14 +338,18 @@ struct hk_ctx {
     bbox_scratch = dmalloc<double>(hk::bbox_scratch_doubles());
     bbox_out = dmalloc<double>(5);
     ck(cudaMallocHost(&h_bbox, 5 * sizeof(double)), "cudaMallocHost");
-    if (g == 1) return;
+    // HK_FORCE_NCCL=1: the NCCL data plane even for one device (a one-rank
+    // communicator: exercises the all-gather / broadcast path on one GPU)
+    const char* force = std::getenv("HK_FORCE_NCCL");
+    const bool force_nccl = force && std::atoi(force) != 0;
+    if (g == 1 && !force_nccl) return;
     std::vector<int> ids(g);
     for (int k = 0; k < g; ++k) ids[k] = devs[k].dev;
     std::vector<int> sorted_ids = ids;
     std::sort(sorted_ids.begin(), sorted_ids.end());
     const bool distinct = std::adjacent_find(sorted_ids.begin(), sorted_ids.end()) == sorted_ids.end();
     const char* no = std::getenv("HK_NO_NCCL");
-    use_nccl = distinct && !(no && std::atoi(no) != 0);
+    use_nccl = distinct && (force_nccl || !(no && std::atoi(no) != 0));
     for (auto& s : devs) {
       ck(cudaSetDevice(s.dev), "cudaSetDevice");
       s.gather6 = dmalloc<double>(6 * static_cast<std::size_t>(g));
@@ -368,7 +376,7 @@ struct hk_ctx {
     ck(cudaMemcpyAsync(h_bbox, bbox_out, 5 * sizeof(double), cudaMemcpyDeviceToHost, s0.stream),
        "bbox copy");
     const int g = static_cast<int>(devs.size());
-    if (g > 1) {
+    if (multi()) {
       if (use_nccl) {
         const NcclApi& api = nccl_api();
         nck(api.GroupStart(), "ncclGroupStart");
@@ -824,7 +832,7 @@ struct hk_ctx {
         d_grad = dev_rows[k] + rows;
       }
       expanded[k] = enqueue(s, c, grad, halves, bgi, tri, d_ell, d_grad, &fgt);
-      if (devs.size() == 1)
+      if (!multi())
         ck(cudaMemcpyAsync(s.h_out6, s.out6, 6 * sizeof(double), cudaMemcpyDeviceToHost, s.stream),
            "result copy");
       if (ell_rows)
@@ -837,7 +845,7 @@ struct hk_ctx {
            "rows copy");
       off += rows;
     }
-    if (devs.size() > 1) {
+    if (multi()) {
       reduce_devices();
       ck(cudaSetDevice(devs[0].dev), "cudaSetDevice");
       ck(cudaMemcpyAsync(devs[0].h_out6, devs[0].total6, 6 * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1221,13 +1229,13 @@ int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad) {
       ++ctx->fgt_evals;
       ctx->fgt_pending = true;
     }
-    if (ctx->devs.size() > 1) ctx->reduce_devices();
+    if (ctx->multi()) ctx->reduce_devices();
   });
 }
 
 const double* hk_result_device(hk_ctx* ctx) {
   if (!ctx || ctx->devs.empty()) return nullptr;
-  return ctx->devs.size() > 1 ? ctx->devs[0].total6 : ctx->devs[0].out6;
+  return ctx->multi() ? ctx->devs[0].total6 : ctx->devs[0].out6;
 }
 
 void* hk_stream(hk_ctx* ctx, int dev) {

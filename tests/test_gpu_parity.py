@@ -649,3 +649,29 @@ def test_set_locations_rejects_non_finite_on_device(eng):
         ev.eval(eng.HawkesParams(**BENCH))
     ev.set_locations(cat.lon, cat.lat)
     assert ev.eval(eng.HawkesParams(**BENCH)) == eng.Evaluator(cat).eval(eng.HawkesParams(**BENCH))
+
+
+def test_nccl_data_plane_one_device(eng, monkeypatch):
+    """The C-ABI's NCCL data plane on one GPU (HK_FORCE_NCCL=1: a one-rank
+    communicator): the 6-vector goes through ncclAllGather + the device-order
+    sum, locations through ncclBroadcast; bitwise the plain context's result
+    (libnccl.so.2 is dlopen'ed by the library, here torch's copy)."""
+    import torch
+    from paper_2407_11349_b200.dist import _DeviceView
+    cat = eng.benchmark_catalog(30000, 23)
+    p = hp(eng, BENCH, 1)
+    plain = eng.Evaluator(cat)
+    monkeypatch.setenv("HK_FORCE_NCCL", "1")
+    ev = eng.Evaluator(cat, devices=[0], plan_for=1)
+    a, b = plain.eval(p, grad=True), ev.eval(p, grad=True)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1])
+    rng = np.random.default_rng(8)
+    lon, lat = rng.uniform(-5, 5, 30000), rng.uniform(-5, 5, 30000)
+    plain.set_locations(lon, lat)
+    ev.set_locations(lon, lat)
+    a, b = plain.eval(p, grad=True), ev.eval(p, grad=True)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1])
+    ev.eval_async(p, True)
+    torch.cuda.synchronize()
+    res = torch.as_tensor(_DeviceView(ev.result_device_ptr(), 6), device="cuda").cpu()
+    assert float(res[0]) == a[0]
