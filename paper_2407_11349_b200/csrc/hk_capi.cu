@@ -916,6 +916,13 @@ struct hk_ctx {
 
 namespace {
 
+// Per-row trigger weight of the shard cost model (hk_host.hpp).
+double shard_beta(int variant, std::size_t n) {
+  if (variant == HK_VARIANT_VARYING) return hk::kCostBetaVarying;
+  if (n >= hk::kFgtPlanRows) return hk::kCostBetaFgt;
+  return n >= hk::kExpansionRows ? hk::kCostBetaExpanded : hk::kCostBeta;
+}
+
 std::unique_ptr<hk_ctx> new_ctx(const double* t, const double* x, const double* y,
                                 const double* d, std::size_t n) {
   if (!t || !x || !y || !d) throw std::invalid_argument("hk_create: null array");
@@ -970,10 +977,7 @@ int create_on(const double* t, const double* lon, const double* lat, const doubl
     if (*std::min_element(devices, devices + n_dev) < 0)
       throw std::invalid_argument("hk_create: negative device index");
     if (static_cast<std::size_t>(n_dev) > n) throw std::invalid_argument("Partition: more workers than terms");
-    const double beta = variant == HK_VARIANT_VARYING ? hk::kCostBetaVarying
-                        : n >= hk::kExpansionRows        ? hk::kCostBetaExpanded
-                                                         : hk::kCostBeta;
-    const auto bounds = hk::plan_shards(ctx->lb, static_cast<std::size_t>(n_dev), beta);
+    const auto bounds = hk::plan_shards(ctx->lb, static_cast<std::size_t>(n_dev), shard_beta(variant, n));
     ctx->devs.resize(n_dev);
     for (int i = 0; i < n_dev; ++i)
       ctx->init_device(ctx->devs[i], devices[i], static_cast<int>(bounds[i]), static_cast<int>(bounds[i + 1]));
@@ -1434,10 +1438,7 @@ int hk_plan_shards_variant(const double* t, size_t n, size_t g, int variant, siz
         throw std::invalid_argument("Catalog: times not sorted at index " + std::to_string(i));
     std::vector<int> lb, ub;
     hk::tie_bounds(tv, lb, ub);
-    const double beta = variant == HK_VARIANT_VARYING ? hk::kCostBetaVarying
-                        : n >= hk::kExpansionRows        ? hk::kCostBetaExpanded
-                                                         : hk::kCostBeta;
-    const auto b = hk::plan_shards(lb, g, beta);
+    const auto b = hk::plan_shards(lb, g, shard_beta(variant, n));
     std::copy(b.begin(), b.end(), bounds);
   });
 }

@@ -49,6 +49,13 @@ constexpr double kCostBeta = 16.0;           // FP64 per trigger pair (direct ba
 // column.
 constexpr double kCostBetaExpanded = 46.0;
 constexpr std::size_t kExpansionRows = 32768;  // catalogs at least this large expand
+// From this size the homogeneous trigger before each checkpoint and the
+// background go through the Hermite expansions (hk_fgt.cu, on by default):
+// every row then costs about the same (the expansion's row evaluation is
+// independent of t_i and the direct remainder is bounded by a checkpoint's
+// width), so homogeneous shards are planned with beta = 0 (equal rows).
+constexpr std::size_t kFgtPlanRows = 131072;
+constexpr double kCostBetaFgt = 0.0;
 inline double background_cost(std::size_t n) {
   return n >= kExpansionRows ? kCostAlphaExpanded : kCostAlphaDirect;
 }

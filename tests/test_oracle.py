@@ -67,9 +67,18 @@ def test_plan_shards_balanced():
     for g in (1, 2, 4, 8):
         b = plan_shards(t, g)
         assert b[0] == 0 and b[-1] == len(t) and np.all(np.diff(b) > 0)
-        cost = 1.0 * (len(t) - 1) + 46.0 * lb  # N >= 32768: expanded background
+        # N >= 131072: the Hermite expansions make every homogeneous row cost the
+        # same (hk_host.hpp kCostBetaFgt): equal rows
+        assert np.diff(b).max() - np.diff(b).min() <= 1
+    t = benchmark_catalog(100000, 42).t
+    lb = np.searchsorted(t, t, side="left")
+    for g in (2, 4, 8):
+        b = plan_shards(t, g)
+        cost = 1.0 * (len(t) - 1) + 46.0 * lb  # 32768 <= N < 131072: expanded background
         w = np.array([cost[b[i]:b[i + 1]].sum() for i in range(g)])
         assert w.max() / w.mean() < 1.001
+    t = benchmark_catalog(200000, 42).t
+    lb = np.searchsorted(t, t, side="left")
     # the density-scaled kernel's culled trigger weighs 4.3 per earlier row
     for g in (2, 8):
         b = plan_shards(t, g, 1)
