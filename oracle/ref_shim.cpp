@@ -14,7 +14,7 @@
 //   slice_log_likelihood       engine.hpp:65-83
 //   event_contribution         model.hpp:225-230
 //   naive_log_likelihood       simulate.hpp:121-136
-//   pair_rate / integral_term  model.hpp:234-250 / :301-306
+//   pair_rate / integral_term  model.hpp:234-250 / :175-180
 //   gaussian_pdf / gaussian_cdf model.hpp:27-34
 //   LikelihoodWorkspace<double> engine.hpp:117-229
 #include <cmath>

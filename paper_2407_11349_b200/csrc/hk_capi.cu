@@ -158,8 +158,10 @@ struct DeviceState {
   // work plans per variant (rows per item differ, hk_device.cuh)
   // plans: [0] constant (also every background-only launch of the varying
   // variant, see enqueue), [1] varying (clustered windows)
-  hk::Item* items[2] = {nullptr, nullptr};
-  int n_items[2] = {0, 0}, slots[2] = {0, 0};
+  // [2]: the homogeneous trigger-only plan with the Hermite expansion
+  // (hk_host.cpp plan_items_fgt: one item per row block over its band)
+  hk::Item* items[3] = {nullptr, nullptr, nullptr};
+  int n_items[3] = {0, 0, 0}, slots[3] = {0, 0, 0};
   double* partial = nullptr;
   double* bg_sums[2] = {nullptr, nullptr};  // [B, B2] x rows, LRU-2 (workspace cache)
   double* tr_sums[2] = {nullptr, nullptr};  // [T, Td, Tq] x rows
@@ -464,6 +466,14 @@ struct hk_ctx {
                     cudaMemcpyHostToDevice),
          "upload items");
     }
+    {
+      std::vector<hk::Item> items;
+      s.slots[2] = hk::plan_items_fgt(lb, ub, n, rb, re, hk::rows_per_item(false), items);
+      s.n_items[2] = static_cast<int>(items.size());
+      s.items[2] = dmalloc<hk::Item>(items.size());
+      ck(cudaMemcpy(s.items[2], items.data(), items.size() * sizeof(hk::Item), cudaMemcpyHostToDevice),
+         "upload items");
+    }
     const std::size_t rows = static_cast<std::size_t>(re - rb);
     {  // Hermite-expansion checkpoints of the homogeneous plan (hk_host.cpp plan_items: Item::xt)
       static_assert(hk::kFgtRowBlock == hk::rows_per_item(false), "FGT checkpoints follow the homogeneous plan");
@@ -488,7 +498,8 @@ struct hk_ctx {
       for (int b = 0; b < nblocks; ++b)
         s.fgt_direct_cost += static_cast<double>(std::min(bi, re - rb - b * bi)) * ckp[b / hk::kFgtBlocks];
     }
-    s.partial = dmalloc<double>(static_cast<std::size_t>(std::max(s.slots[0], s.slots[1])) * 5 * rows);
+    s.partial = dmalloc<double>(static_cast<std::size_t>(std::max({s.slots[0], s.slots[1], s.slots[2]})) * 5 *
+                                rows);
     for (int k = 0; k < 2; ++k) {
       s.bg_sums[k] = dmalloc<double>(2 * rows);
       s.tr_sums[k] = dmalloc<double>(3 * rows);
@@ -740,6 +751,9 @@ struct hk_ctx {
     if (halves) {
       hk::launch_prep(dc, c, s.stream);
       const int v = c.varying ? 1 : 0;
+      // the pair launch's plan: the expansion's band-only plan when it computes
+      // just the homogeneous trigger next to the expansion
+      const int pv = (use_fgt && halves == hk::kHalfTr) ? 2 : v;
       // The density-scaled kernel's rows come in clustered windows that span
       // far more time than a row block, which would disqualify the
       // background block expansion.  The background does not depend on the
@@ -765,7 +779,7 @@ struct hk_ctx {
       } else {
         const int kind = halves == (hk::kHalfBg | hk::kHalfTr) ? 0 : (halves == hk::kHalfBg ? 1 : 2);
         timed_pair(s, kind, [&] {
-          hk::launch_pair(dc, c, s.items[v], s.n_items[v], s.partial, s.rb, rows, grad, halves, s.stream,
+          hk::launch_pair(dc, c, s.items[pv], s.n_items[pv], s.partial, s.rb, rows, grad, halves, s.stream,
                           use_fgt);
         });
       }
@@ -776,7 +790,7 @@ struct hk_ctx {
           hk::launch_collapse(s.partial, s.slots[1], rows, nullptr, s.tr_sums[tri], s.stream);
         prof_total += (halves == (hk::kHalfBg | hk::kHalfTr)) ? 5 : 3;
       } else {
-        hk::launch_collapse(s.partial, s.slots[v], rows,
+        hk::launch_collapse(s.partial, s.slots[pv], rows,
                             (halves & hk::kHalfBg) ? s.bg_sums[bgi] : nullptr,
                             (halves & hk::kHalfTr) ? s.tr_sums[tri] : nullptr, s.stream);
         prof_total += 3;

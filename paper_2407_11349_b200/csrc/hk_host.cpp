@@ -233,6 +233,42 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
   return slots;
 }
 
+int plan_items_fgt(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
+                   int kBI, std::vector<Item>& items) {
+  items.clear();
+  const int ntiles = (n + kBJ - 1) / kBJ;
+  const int nblocks = (re - rb + kBI - 1) / kBI;
+  struct Span {
+    int r0, r1, tb, te;
+  };
+  std::vector<Span> spans(nblocks);
+  int max_tiles = 1;
+  for (int b = 0; b < nblocks; ++b) {
+    const int r0 = rb + b * kBI, r1 = std::min(re, r0 + kBI);
+    const int xt = lb[rb + (b / kFgtBlocks) * kFgtBlocks * kBI] / kBJ;  // as plan_items' Item::xt
+    const int te = std::min(ntiles, (ub[r1 - 1] + kBJ - 1) / kBJ);     // beyond: background only
+    spans[b] = {r0, r1, xt, std::max(te, xt + 1)};
+    max_tiles = std::max(max_tiles, spans[b].te - spans[b].tb);
+  }
+  const int slots = (max_tiles + kMaxItemTiles - 1) / kMaxItemTiles;
+  struct Cand {
+    Item it;
+    double cost;
+  };
+  std::vector<Cand> cands;
+  for (const Span& sp : spans) {
+    const int per = (sp.te - sp.tb + slots - 1) / slots;
+    for (int c = 0; c < slots; ++c) {
+      const int tb = std::min(sp.te, sp.tb + c * per), te = std::min(sp.te, tb + per);
+      cands.push_back({Item{sp.r0, sp.r1, tb, std::max(te, tb), c, -1, sp.tb},
+                       static_cast<double>(te - tb) * (sp.r1 - sp.r0)});
+    }
+  }
+  std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.cost > b.cost; });
+  for (const auto& c : cands) items.push_back(c.it);
+  return slots;
+}
+
 EvalCoef make_coef(const ParamsIn& p, double t_min, double t_max, double d2_max, double q_max) {
   EvalCoef c{};
   c.mu0 = p.mu0;

@@ -75,6 +75,14 @@ std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g,
 int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
                int rows_per_item, std::vector<Item>& items, int window = 1);
 
+// The homogeneous plan when the pair kernel computes only the trigger and the
+// Hermite expansion supplies every tile below each block's checkpoint: one
+// item per row block (more only if a block's remaining band exceeds
+// kMaxItemTiles tiles) over the tiles [checkpoint, last tile of the block's
+// ties).  Returns the slots (chunks per block).
+int plan_items_fgt(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
+                   int kBI, std::vector<Item>& items);
+
 // Per-evaluation coefficients (types.hpp:105-109, model.hpp:202-210) and
 // the host-side argument bound that selects the checked exp.
 EvalCoef make_coef(const ParamsIn& p, double t_min, double t_max, double d2_max, double q_max);

@@ -357,7 +357,7 @@ constexpr float kEx2Shift = 24.0f;
 constexpr double kEx2Unscale = 5.9604644775390625e-08;  // 2^-24
 
 // Precision::single trigger of a BT/BTx/T tile (the reference's float path,
-// model.hpp:57-82 / :271-296, evaluated with MUFU ex2): FP32 distances in
+// model.hpp:57-82 / :145-170, evaluated with MUFU ex2): FP32 distances in
 // the centred frame, FP32 partial sums within the tile, then the FP64 row
 // factor exp(-omega (t_i - t_ref)) and an FP64 accumulator across tiles.
 template <int NR, bool kVarying, int kMode, bool kC = false>
