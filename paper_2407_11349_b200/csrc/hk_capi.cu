@@ -178,6 +178,8 @@ struct DeviceState {
   int* fgt_box = nullptr;                                // [fgt_cols]
   double *fgt_u = nullptr, *fgt_v = nullptr;             // [fgt_cols]
   double* fgt_mom = nullptr;                             // [nck][nbox][2][P^2], grown on demand
+  int* fgt_perm = nullptr;                               // [nck * kFgtCkRows] clustered rows
+  long fgt_perm_loc = -1;                                // location version of fgt_perm
   std::size_t fgt_mom_bytes = 0;
   double* bgf_mom = nullptr;  // [nbt][kFgtP]: the background's 1-D expansion
   int* bgf_count = nullptr;   // [nbt]
@@ -281,7 +283,8 @@ struct hk_ctx {
       for (void* q : {static_cast<void*>(s.ck_P), static_cast<void*>(s.fgt_tR), static_cast<void*>(s.fgt_decay),
                       static_cast<void*>(s.fgt_dt), static_cast<void*>(s.fgt_box), static_cast<void*>(s.fgt_u),
                       static_cast<void*>(s.fgt_v), static_cast<void*>(s.fgt_mom), static_cast<void*>(s.fgt_flag),
-                      static_cast<void*>(s.bgf_mom), static_cast<void*>(s.bgf_count), static_cast<void*>(s.fgt_wsum)})
+                      static_cast<void*>(s.bgf_mom), static_cast<void*>(s.bgf_count), static_cast<void*>(s.fgt_wsum),
+                      static_cast<void*>(s.fgt_perm)})
         if (q) cudaFree(q);
       if (s.h_fgt_flag) cudaFreeHost(s.h_fgt_flag);
       if (s.gather6) cudaFree(s.gather6);
@@ -489,6 +492,8 @@ struct hk_ctx {
       s.fgt_decay = dmalloc<double>(s.nck);
       s.fgt_dt = dmalloc<double>(s.nck);
       s.fgt_wsum = dmalloc<double>(s.nck);
+      s.fgt_perm = dmalloc<int>(static_cast<std::size_t>(s.nck) * hk::kFgtCkRows);
+      static_assert((hk::kFgtCkRows & (hk::kFgtCkRows - 1)) == 0, "checkpoint windows are sorted bitonically");
       s.fgt_box = dmalloc<int>(s.fgt_cols);
       s.fgt_u = dmalloc<double>(s.fgt_cols);
       s.fgt_v = dmalloc<double>(s.fgt_cols);
@@ -644,6 +649,7 @@ struct hk_ctx {
     F.v = s.fgt_v;
     F.mom = s.fgt_mom;
     F.wsum = s.fgt_wsum;
+    F.perm = s.fgt_perm;
     return F;
   }
 
@@ -744,6 +750,12 @@ struct hk_ctx {
     }
     hk::FgtParams F{};
     if (use_fgt) {
+      if (s.fgt_perm_loc != loc_version) {  // checkpoint rows in spatial order, once per location set
+        hk::launch_cluster(s.x, s.y, s.fgt_perm, s.rb, rows, hk::kFgtCkRows, s.nck, hk::kFgtLeaf, cx, cy,
+                           half_extent, s.stream, hk::kFgtCkRows);
+        s.fgt_perm_loc = loc_version;
+        prof_total += 1;
+      }
       F = fgt_params(s, c, *fgt, grad);
       timed_pair(s, 3, [&] { hk::launch_fgt_prepare(F, s.stream); });
       prof_total += 4;

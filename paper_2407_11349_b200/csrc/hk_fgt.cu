@@ -242,20 +242,25 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 2)
   constexpr unsigned kBoxBytes = kSets * PP * sizeof(double);
   __shared__ __align__(128) double s_m[2][kSets * PP];
   __shared__ __align__(8) uint64_t s_bar[2];
+  // positions in the checkpoint's spatially clustered order (cluster_kernel,
+  // windows = checkpoints, leaves = one warp's kFgtLeaf rows): a warp's rows
+  // are close together, so boxes beyond the cut-off of all of them are skipped
   const int cta_rows = R * kFgtEvalThreads;
-  const int row_block = (blockIdx.x * cta_rows) / kFgtRowBlock;
-  const int k = row_block / kFgtBlocks;
+  const int k = (blockIdx.x * cta_rows) / kFgtCkRows;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int li[R];
   bool valid[R];
   double xi[R], yi[R], ti[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    li[r] = blockIdx.x * cta_rows + r * kFgtEvalThreads + threadIdx.x;
-    valid[r] = li[r] < rows_total;
-    const int row = rows_base + (valid[r] ? li[r] : rows_total - 1);
-    xi[r] = F.x[row];
-    yi[r] = F.y[row];
-    ti[r] = F.t[row];
+    const int pos = blockIdx.x * cta_rows + warp * kFgtLeaf + r * 32 + lane;
+    const int row = F.perm[pos];
+    valid[r] = row >= 0;
+    li[r] = valid[r] ? row - rows_base : 0;
+    const int rr = valid[r] ? row : rows_base;
+    xi[r] = F.x[rr];
+    yi[r] = F.y[rr];
+    ti[r] = F.t[rr];
   }
   const double* mk = F.mom + static_cast<size_t>(k) * F.nbox * 2 * PP;
   if (threadIdx.x == 0) {
@@ -324,14 +329,22 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 2)
             const double2 ab = *reinterpret_cast<const double2*>(Ar + b);
             double2 bb;
             if (kGrad) bb = *reinterpret_cast<const double2*>(Ar + PP + b);
+            // the b terms of every chain first, then the b+1 terms: each
+            // accumulator's dependent multiply-adds are 2 R (grad: 3 R) - 1
+            // independent ones apart (the DFMA latency is hidden in-thread)
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               sA[r] = fma(ab.x, hy[r][b], sA[r]);
-              sA[r] = fma(ab.y, hy[r][b + 1], sA[r]);
               if (kGrad) {
                 sA2[r] = fma(ab.x, hy[r][b + 2], sA2[r]);
-                sA2[r] = fma(ab.y, hy[r][b + 3], sA2[r]);
                 sB[r] = fma(bb.x, hy[r][b], sB[r]);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+              sA[r] = fma(ab.y, hy[r][b + 1], sA[r]);
+              if (kGrad) {
+                sA2[r] = fma(ab.y, hy[r][b + 3], sA2[r]);
                 sB[r] = fma(bb.y, hy[r][b + 1], sB[r]);
               }
             }
@@ -553,7 +566,7 @@ void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* 
 void launch_fgt_eval(const FgtParams& F, int rows_base, int rows_total, const double* bg_sums,
                      double* tr_sums, double coef_a, double coef_c, unsigned* flag, cudaStream_t s) {
   const int rows_per_cta = kFgtRowsPerThread * kFgtEvalThreads;
-  const int blocks = (rows_total + rows_per_cta - 1) / rows_per_cta;
+  const int blocks = F.nck * (kFgtCkRows / rows_per_cta);  // the permutation's positions
   if (F.grad)
     fgt_eval_kernel<true><<<blocks, kFgtEvalThreads, 0, s>>>(F, rows_base, rows_total, bg_sums, tr_sums,
                                                              coef_a, coef_c, flag);

@@ -11,7 +11,9 @@ constexpr int kFgtBlocks = 4;          // homogeneous row blocks per checkpoint
 constexpr int kFgtRowBlock = 512;      // rows per block of the homogeneous plan (rows_per_item(false))
 constexpr int kFgtEvalThreads = 128;   // threads per evaluation CTA
 constexpr int kFgtRowsPerThread = 2;   // rows per thread (kFgtEvalThreads x this divides kFgtRowBlock)
-constexpr double kFgtCut = 46.0;       // boxes farther than sqrt(46) scaled units are skipped
+constexpr int kFgtCkRows = kFgtBlocks * kFgtRowBlock;  // rows per checkpoint (a power of two)
+constexpr int kFgtLeaf = 32 * kFgtRowsPerThread;       // one warp's rows: a k-d leaf
+constexpr double kFgtCut = 36.0;       // boxes farther than 6 scaled units are skipped (<= e^-36 per unit weight)
 constexpr double kFgtRowTol = 1e-13;   // certified per-row relative error bound, else recompute directly
 constexpr int kFgtMaxBoxes = 1024;     // larger grids (small sigma_x / wide catalogs): direct path
 
@@ -33,6 +35,7 @@ struct FgtParams {
   double *u, *v;                // [ncols] scaled offsets from the box centre
   double* mom;                  // [nck][nbox][2][kFgtP^2]: A (and B) moments
   double* wsum;                 // [nck] total prefix weight (sum over boxes of A_00)
+  const int* perm;              // [nck * kFgtCkRows] each checkpoint's rows in spatial (k-d) order, -1: none
 };
 
 // The background's 1-D expansion in time (hk_fgt.cu, both variants).

@@ -830,14 +830,15 @@ __device__ __forceinline__ unsigned quantise16(double v, double c, double inv_ex
 __global__ void __launch_bounds__(kClusterThreads)
     cluster_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm,
                    int rows_base, int rows, int window, int n_windows, int leaf, double cx,
-                   double cy, double inv_extent) {
+                   double cy, double inv_extent, int kBI) {
   // dynamic shared memory (aliases the exp table of other kernels): packed
   // keys (x << 16 | y) and row indices within the window
   unsigned* kxy = reinterpret_cast<unsigned*>(s_exp2_tab);
   unsigned short* kv = reinterpret_cast<unsigned short*>(kxy + window);
   // window blockIdx.x: rows [w0, w1) of the shard, sorted into rperm slots
   // [blockIdx.x * window, + window)
-  constexpr int kBI = kThreads * rows_per_thread(true);
+  // windows are whole groups of kBI-row blocks (the varying plan's 256-row
+  // blocks, or the trigger expansion's 2048-row checkpoints)
   const int nblocks = (rows + kBI - 1) / kBI;
   const int w0 = window_first_block(blockIdx.x, nblocks, n_windows) * kBI;
   const int w1 = min(rows, window_first_block(blockIdx.x + 1, nblocks, n_windows) * kBI);
@@ -1105,7 +1106,7 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
 
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, double half_extent,
-                    cudaStream_t s) {
+                    cudaStream_t s, int block_rows) {
   if (rows <= 0 || n_windows <= 0) return;
   if (window > kMaxClusterWindow || window < leaf || window % leaf)
     throw std::invalid_argument("launch_cluster: unsupported window of " + std::to_string(window) +
@@ -1114,7 +1115,8 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
   const double inv_extent = half_extent > 0.0 ? 1.0 / half_extent : 0.0;
   cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cluster_kernel<<<n_windows, kClusterThreads, bytes, s>>>(x, y, rperm, rows_base, rows, window,
-                                                           n_windows, leaf, cx, cy, inv_extent);
+                                                           n_windows, leaf, cx, cy, inv_extent,
+                                                           block_rows > 0 ? block_rows : rows_per_item(true));
 }
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,

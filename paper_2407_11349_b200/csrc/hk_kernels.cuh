@@ -89,9 +89,10 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
 // of few rows would cluster badly.  Any order gives bitwise the same per-row
 // sums: the clustering only lets the density-scaled trigger skip columns per
 // warp.
+// block_rows: the row blocks windows are made of (0: the varying plan's).
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, double half_extent,
-                    cudaStream_t s);
+                    cudaStream_t s, int block_rows = 0);
 constexpr int kMaxClusterWindow = 32768;  // rows (6 bytes each: 192 KB of dynamic shared memory)
 // Windows of at most max_blocks row blocks covering nblocks: their number,
 // the first block of window w, and the window of block b.
