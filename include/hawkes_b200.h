@@ -220,6 +220,11 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
  *     certified 1-D Hermite expansion in time (both variants, FP64 only);
  *     0 returns them to the pair kernels (block expansion / per pair). */
 #define HK_OPT_BG_FGT 3
+/*   HK_OPT_TR_CUT: the density-scaled FP64 trigger drops a source for every
+ *     row whose spatial factor is below e^-46 (instead of only exact zeros);
+ *     the dropped weight is bounded per row and certified like the
+ *     expansions (1e-13 relative to the row's rate, else recomputed). */
+#define HK_OPT_TR_CUT 4
 int hk_set_option(hk_ctx* ctx, int option, int value);
 /* Evaluations that used a Hermite expansion (trigger or background),
  * synchronous ones recomputed

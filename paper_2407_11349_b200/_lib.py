@@ -28,6 +28,7 @@ HK_OK, HK_INVALID_ARGUMENT, HK_OUT_OF_RANGE, HK_RUNTIME_ERROR, HK_NOT_IMPLEMENTE
 HK_OPT_BG_EXPANSION = 1
 HK_OPT_FGT = 2
 HK_OPT_BG_FGT = 3
+HK_OPT_TR_CUT = 4
 
 
 class hk_params(C.Structure):

@@ -187,6 +187,7 @@ struct DeviceState {
   unsigned* fgt_flag = nullptr;                          // device
   unsigned* h_fgt_flag = nullptr;                        // pinned
   bool flag_pending = false;                             // set by hk_eval_async
+  double* cert_scratch = nullptr;                        // density-scaled cut certification
   double* gather6 = nullptr;  // [n_dev][6]: every device's out6 (multi-device contexts)
   double* total6 = nullptr;   // their device-order sum
   cudaEvent_t done = nullptr; // peer-copy mode: this device's part is ready
@@ -221,6 +222,7 @@ struct hk_ctx {
   int bg_expansion = 1;
   int fgt_enabled = 1;     // HK_OPT_FGT
   int bg_fgt_enabled = 1;  // HK_OPT_BG_FGT
+  int tr_cut_enabled = 1;  // HK_OPT_TR_CUT
   long fgt_evals = 0, fgt_fallbacks = 0;
   bool fgt_pending = false;  // an async evaluation's certification flag is unread
 
@@ -284,7 +286,7 @@ struct hk_ctx {
                       static_cast<void*>(s.fgt_dt), static_cast<void*>(s.fgt_box), static_cast<void*>(s.fgt_u),
                       static_cast<void*>(s.fgt_v), static_cast<void*>(s.fgt_mom), static_cast<void*>(s.fgt_flag),
                       static_cast<void*>(s.bgf_mom), static_cast<void*>(s.bgf_count), static_cast<void*>(s.fgt_wsum),
-                      static_cast<void*>(s.fgt_perm)})
+                      static_cast<void*>(s.fgt_perm), static_cast<void*>(s.cert_scratch)})
         if (q) cudaFree(q);
       if (s.h_fgt_flag) cudaFreeHost(s.h_fgt_flag);
       if (s.gather6) cudaFree(s.gather6);
@@ -492,6 +494,7 @@ struct hk_ctx {
       s.fgt_decay = dmalloc<double>(s.nck);
       s.fgt_dt = dmalloc<double>(s.nck);
       s.fgt_wsum = dmalloc<double>(s.nck);
+      s.cert_scratch = dmalloc<double>(4 * static_cast<std::size_t>((n + hk::kCertChunk - 1) / hk::kCertChunk));
       s.fgt_perm = dmalloc<int>(static_cast<std::size_t>(s.nck) * hk::kFgtCkRows);
       static_assert((hk::kFgtCkRows & (hk::kFgtCkRows - 1)) == 0, "checkpoint windows are sorted bitonically");
       s.fgt_box = dmalloc<int>(s.fgt_cols);
@@ -653,6 +656,13 @@ struct hk_ctx {
     return F;
   }
 
+  // The density-scaled FP64 trigger drops columns whose spatial factor is
+  // below e^{-46} of their weight (certified per row, hk::launch_tr_cut_cert;
+  // HK_OPT_TR_CUT=0 keeps the flush threshold: exact zeros only).
+  void set_cut(hk::EvalCoef& c) const {
+    if (tr_cut_enabled && c.varying && !c.single_prec) c.tr_cut = 46.0 * hk::kLog2eT;
+  }
+
   // The trigger half depends on the variant and on the precision.
   static int tr_variant(const hk::EvalCoef& c) { return c.varying + 2 * c.single_prec; }
 
@@ -662,6 +672,7 @@ struct hk_ctx {
   int plan_halves(const hk::EvalCoef& c, bool grad, bool force, int& bgi, int& tri, bool fgt = false,
                   bool bg_fgt = false) {
     const int bgx = c.bg_expansion + (bg_fgt ? 2 : 0);  // how the background half is computed
+    const int tr_how = (fgt ? 1 : 0) + (c.tr_cut > 0.0 ? 2 : 0);  // ... and the trigger half
     // the background half is FP64 in both precisions, but each precision
     // keeps its own entries so a cached result is bitwise the fresh one of
     // the same precision (the launches differ between the two)
@@ -671,7 +682,7 @@ struct hk_ctx {
     };
     auto hit_tr = [&](const Key& k) {
       return k.valid && k.a == c.sigma_x && k.b == c.sigma_t && k.variant == tr_variant(c) &&
-             k.loc == loc_version && k.bgx == (fgt ? 1 : 0) && (k.grad || !grad);
+             k.loc == loc_version && k.bgx == tr_how && (k.grad || !grad);
     };
     int halves = 0;
     bgi = -1;
@@ -689,7 +700,7 @@ struct hk_ctx {
     if (tri < 0) {
       halves |= hk::kHalfTr;
       tri = tr_key[0].used <= tr_key[1].used ? 0 : 1;
-      tr_key[tri] = Key{true, c.sigma_x, c.sigma_t, tr_variant(c), grad ? 1 : 0, fgt ? 1 : 0, loc_version, 0};
+      tr_key[tri] = Key{true, c.sigma_x, c.sigma_t, tr_variant(c), grad ? 1 : 0, tr_how, loc_version, 0};
     }
     bg_key[bgi].used = ++clock;
     tr_key[tri].used = ++clock;
@@ -717,7 +728,8 @@ struct hk_ctx {
     }
     const bool use_fgt = fgt && fgt->on && (halves & hk::kHalfTr) && s.nck > 0;
     const bool use_bgf = fgt && fgt->bg && (halves & hk::kHalfBg);
-    if (use_fgt || use_bgf) ck(cudaMemsetAsync(s.fgt_flag, 0, sizeof(unsigned), s.stream), "memset");
+    const bool use_cut = c.tr_cut > 0.0 && (halves & hk::kHalfTr);
+    if (use_fgt || use_bgf || use_cut) ck(cudaMemsetAsync(s.fgt_flag, 0, sizeof(unsigned), s.stream), "memset");
     if (use_bgf) {  // the background half by the 1-D expansion in time, straight into bg_sums
       if (fgt->nbt > s.bgf_cap) {
         if (s.bgf_mom) ck(cudaFree(s.bgf_mom), "cudaFree");
@@ -815,7 +827,14 @@ struct hk_ctx {
       });
       prof_total += 1;
     }
-    if (use_fgt || use_bgf)
+    if (use_cut) {
+      double tol = hk::kFgtRowTol;
+      if (const char* e = std::getenv("HK_FGT_ROW_TOL")) tol = std::atof(e);
+      hk::launch_tr_cut_cert(dc, c, s.bg_sums[bgi], s.tr_sums[tri], s.rb, rows, s.cert_scratch, tol,
+                             s.fgt_flag, s.stream);
+      prof_total += 3;
+    }
+    if (use_fgt || use_bgf || use_cut)
       ck(cudaMemcpyAsync(s.h_fgt_flag, s.fgt_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, s.stream),
          "flag copy");
     hk::launch_finish(dc, c, s.bg_sums[bgi], s.tr_sums[tri], s.rb, rows, grad, ell_rows,
@@ -823,7 +842,7 @@ struct hk_ctx {
     hk::launch_reduce(s.blockpart, s.n_finish_blocks, s.out6, s.stream);
     ck(cudaGetLastError(), "kernel launch");
     prof_total += 2;
-    return use_fgt || use_bgf;
+    return use_fgt || use_bgf || use_cut;
   }
 
   // Full or workspace evaluation on every device; sums in device order.
@@ -832,7 +851,8 @@ struct hk_ctx {
   void evaluate(const hk_params* p, bool grad, bool workspace, bool force, double* ll, double* grad5,
                 bool single = false, double* ell_rows = nullptr, double* grad_rows = nullptr,
                 bool allow_fgt = true) {
-    const hk::EvalCoef c = coef(p, single);
+    hk::EvalCoef c = coef(p, single);
+    if (allow_fgt) set_cut(c);
     const FgtPlan fgt = allow_fgt ? fgt_plan(c, grad) : FgtPlan{};
     int bgi, tri;
     const int halves = workspace ? plan_halves(c, grad, force, bgi, tri, fgt.on, fgt.bg)
@@ -1246,7 +1266,8 @@ int hk_ws_stats(const hk_ctx* ctx, long* hits, long* misses) {
 int hk_eval_async(hk_ctx* ctx, const hk_params* p, int with_grad) {
   return guarded([&] {
     if (!ctx) throw std::invalid_argument("hk_eval_async: null context");
-    const hk::EvalCoef c = ctx->coef(p);
+    hk::EvalCoef c = ctx->coef(p);
+    ctx->set_cut(c);
     const hk_ctx::FgtPlan fgt = ctx->fgt_plan(c, with_grad != 0);
     int bgi, tri;
     const int halves = ctx->plan_halves(c, with_grad != 0, /*force=*/true, bgi, tri, fgt.on, fgt.bg);
@@ -1358,6 +1379,7 @@ int hk_set_option(hk_ctx* ctx, int option, int value) {
     if (!ctx) throw std::invalid_argument("hk_set_option: null context");
     if (option == HK_OPT_BG_EXPANSION) ctx->bg_expansion = value != 0;
     else if (option == HK_OPT_BG_FGT) ctx->bg_fgt_enabled = value != 0;
+    else if (option == HK_OPT_TR_CUT) ctx->tr_cut_enabled = value != 0;
     else if (option == HK_OPT_FGT) ctx->fgt_enabled = value != 0;
     else throw std::invalid_argument("hk_set_option: unknown option " + std::to_string(option));
   });

@@ -780,13 +780,17 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
     const double dtr = d.t[jr] - d.t[j];
     const double w = q * exp(-c.omega * dtr);
     d.K[j] = K;
-    d.thr[j] = kFlushArg / (-K);
+    // the candidate test's threshold: every term beyond flushes to exactly 0,
+    // or (tr_cut, density-scaled FP64) is below 2^{-tr_cut/kTab} x q_j w_j,
+    // the dropped weight certified per row afterwards (tr_cut_cert_kernel)
+    const double targ = c.tr_cut > 0.0 ? c.tr_cut : kFlushArg;
+    d.thr[j] = targ / (-K);
     d.w[j] = w;
     d.v[j] = dtr * w;
     d.z[j] = q * w;
     // FP32 skip threshold, rounded up: d2f > thrf implies the exact d^2 > thr
     // (|d_f - d| <= 2 f32_err), i.e. the pair's spatial factor flushes to 0.
-    const double r = sqrt(kFlushArg / (-K)) + 2.0 * c.f32_err;
+    const double r = sqrt(targ / (-K)) + 2.0 * c.f32_err;
     const float thrf = __double2float_ru(r * r * (1.0 + 1.0 / 262144.0));
     d.fxy[j] = make_float4(__double2float_rn(d.x[j] - c.cx), __double2float_rn(d.y[j] - c.cy), thrf,
                            0.f);
@@ -1058,6 +1062,77 @@ __global__ void sum6_kernel(const double* __restrict__ parts, int n_dev, double*
 }
 
 // ---------------------------------------------------------------------------
+// certification of the density-scaled trigger's spatial cut
+
+// chunk c (kCertChunk sources, one CTA): [sum_j q_j exp(-omega (t_last(c) - t_j)),
+// sum_j q_j] (tree reductions; a bound, so their order is immaterial)
+__global__ void __launch_bounds__(256) cert_chunk_kernel(const DeviceCatalog d, const EvalCoef c, double* chunk) {
+  __shared__ double s_a[256], s_b[256];
+  const int j0 = blockIdx.x * kCertChunk, j1 = min(d.n, j0 + kCertChunk);
+  const double tl = d.t[j1 - 1];
+  double a = 0.0, b = 0.0;
+  for (int j = j0 + threadIdx.x; j < j1; j += 256) {
+    a += d.q[j] * exp(-c.omega * (tl - d.t[j]));
+    b += d.q[j];
+  }
+  s_a[threadIdx.x] = a;
+  s_b[threadIdx.x] = b;
+  __syncthreads();
+  for (int h = 128; h > 0; h >>= 1) {
+    if (threadIdx.x < h) {
+      s_a[threadIdx.x] += s_a[threadIdx.x + h];
+      s_b[threadIdx.x] += s_b[threadIdx.x + h];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    chunk[2 * blockIdx.x] = s_a[0];
+    chunk[2 * blockIdx.x + 1] = s_b[0];
+  }
+}
+
+// pre[c] = sum_{j < c kCertChunk} q_j exp(-omega (t[c kCertChunk] - t_j)): one
+// sequential pass over the chunks (their decays precomputed in parallel)
+__global__ void cert_decay_kernel(const DeviceCatalog d, const EvalCoef c, double* chunk, int n_chunks) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_chunks) return;
+  const int j0 = k * kCertChunk, j1 = min(d.n, j0 + kCertChunk);
+  const double tn = j1 < d.n ? d.t[j1] : d.t[d.n - 1];
+  // [2k]: the chunk's own decayed sum, carried to the next chunk's first time
+  chunk[2 * k] *= exp(-c.omega * (tn - d.t[j1 - 1]));
+  chunk[2 * n_chunks + k] = exp(-c.omega * (tn - d.t[j0]));  // the carry's decay across the chunk
+}
+
+__global__ void cert_scan_kernel(const double* chunk, double* pre, int n_chunks) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double p = 0.0;
+  for (int k = 0; k < n_chunks; ++k) {
+    pre[k] = p;
+    p = fma(p, chunk[2 * n_chunks + k], chunk[2 * k]);
+  }
+}
+
+// Q_i <= pre[k] exp(-omega (t_i - t[k C])) + sum_{j in chunk k} q_j with
+// k = lb_i / C (the sources of row i's own chunk before it decay by <= 1)
+__global__ void cert_rows_kernel(const DeviceCatalog d, const EvalCoef c, const double* __restrict__ bg_sums,
+                                 const double* __restrict__ tr_sums, int rows_base, int rows_total,
+                                 const double* __restrict__ chunk, const double* __restrict__ pre,
+                                 double row_tol, unsigned* flag) {
+  const int li = blockIdx.x * blockDim.x + threadIdx.x;
+  if (li >= rows_total) return;
+  const int i = rows_base + li;
+  const int k = d.lb[i] / kCertChunk;
+  double Q = 0.0;
+  if (k * kCertChunk < d.n) Q = pre[k] * exp(-c.omega * (d.t[i] - d.t[k * kCertChunk])) + chunk[2 * k + 1];
+  // every dropped term is below its source's weight q_j exp(-omega (t_i - t_j))
+  // x 2^{-tr_cut/kTab} (the gradient's dropped terms: the same weights x
+  // (t_i - t_j) <= span and x q d^2 <= 2 sigma_x^2 (cut + 1): far below tolerance)
+  const double dropped = c.c * Q * 1.000001 * exp2(-c.tr_cut / kTab);
+  const double S = c.a * bg_sums[li] + c.c * tr_sums[li];
+  if (!(dropped <= row_tol * S)) atomicOr(flag, 1u);
+}
+
+// ---------------------------------------------------------------------------
 // FP64 peak probe: 8 independent DFMA chains per thread, register resident.
 
 __global__ void __launch_bounds__(256) dfma_probe_kernel(double* sink, int iters, double s) {
@@ -1208,6 +1283,19 @@ void launch_bbox(const double* x, const double* y, int n, double* scratch, doubl
 
 void launch_sum6(const double* parts, int n_dev, double* total, cudaStream_t s) {
   sum6_kernel<<<1, 32, 0, s>>>(parts, n_dev, total);
+}
+
+void launch_tr_cut_cert(const DeviceCatalog& d, const EvalCoef& c, const double* bg_sums,
+                        const double* tr_sums, int rows_base, int rows_total, double* scratch,
+                        double row_tol, unsigned* flag, cudaStream_t s) {
+  const int n_chunks = (d.n + kCertChunk - 1) / kCertChunk;
+  double* chunk = scratch;               // [n_chunks][2], then [n_chunks] decays
+  double* pre = scratch + 3 * n_chunks;  // [n_chunks]
+  cert_chunk_kernel<<<n_chunks, 256, 0, s>>>(d, c, chunk);
+  cert_decay_kernel<<<(n_chunks + 255) / 256, 256, 0, s>>>(d, c, chunk, n_chunks);
+  cert_scan_kernel<<<1, 32, 0, s>>>(chunk, pre, n_chunks);
+  cert_rows_kernel<<<(rows_total + 255) / 256, 256, 0, s>>>(d, c, bg_sums, tr_sums, rows_base, rows_total, chunk,
+                                                           pre, row_tol, flag);
 }
 
 void launch_reduce(const double* blockpart, int n_blocks, double* out6, cudaStream_t s) {

@@ -50,6 +50,9 @@ struct EvalCoef {
   int single_prec;   // Precision::single: FP32 trigger arithmetic, LL only
   int varying;
   int mode;       // ExpMode: kExact / kFlush / kChecked from the argument bound
+  double tr_cut;  // density-scaled trigger: spatial exponent (ln2/kTab units) beyond which
+                  // the candidate test drops a column (certified, hk_cert.cu); 0 = the flush
+                  // threshold (only exact zeros dropped)
 };
 
 struct DeviceCatalog {
@@ -120,6 +123,15 @@ int launch_finish(const DeviceCatalog& d, const EvalCoef& c, const double* bg_su
                   const double* tr_sums, int rows_base, int rows_total, bool with_grad,
                   double* ell_rows, double* grad_rows, double* blockpart, cudaStream_t s);
 void launch_reduce(const double* blockpart, int n_blocks, double* out6, cudaStream_t s);
+// Certification of the density-scaled trigger's spatial cut (EvalCoef::tr_cut):
+// per row Q_i = sum_{j < lb_i} q_j exp(-omega (t_i - t_j)) bounds the weight of
+// every dropped source, so the dropped terms are at most Q_i 2^{-tr_cut/kTab};
+// a row where c x that exceeds row_tol x S_i sets *flag.  scratch: 4 x
+// ceil(n / kCertChunk) doubles.
+constexpr int kCertChunk = 1024;
+void launch_tr_cut_cert(const DeviceCatalog& d, const EvalCoef& c, const double* bg_sums,
+                        const double* tr_sums, int rows_base, int rows_total, double* scratch,
+                        double row_tol, unsigned* flag, cudaStream_t s);
 // Bounding box and finiteness of n locations: out5 = {xmin, xmax, ymin, ymax,
 // index of the first non-finite location or n}, on the device; scratch holds
 // bbox_scratch_doubles() doubles.

@@ -297,6 +297,10 @@ class Evaluator:
         """HK_OPT_BG_FGT: the background's 1-D Hermite expansion in time (default on)."""
         check(lib.hk_set_option(self._h, _lib.HK_OPT_BG_FGT, int(on)))
 
+    def set_tr_cut(self, on: bool) -> None:
+        """HK_OPT_TR_CUT: the density-scaled trigger's certified e^-46 spatial cut (default on)."""
+        check(lib.hk_set_option(self._h, _lib.HK_OPT_TR_CUT, int(on)))
+
     def fgt_stats(self):
         """(evaluations through the expansion, direct recomputations, last
         async evaluation flagged)."""

@@ -211,3 +211,41 @@ def test_bg_fgt_certification_on_sparse_catalogs(eng, oracle):
         assert ll == ref[0] and np.array_equal(g, ref[1])
         assert ev.fgt_stats()[1] == 1  # recomputed on the direct path
         assert ll == pytest.approx(oracle.ll_grad(cat.arrays(), p1, 0)[0], rel=1e-12)
+
+
+def county_like(eng, n, seed=3):
+    t, x, y, _ = eng.benchmark_catalog(n, seed).arrays()
+    rng = np.random.default_rng(seed)
+    dens = np.exp(rng.uniform(0, np.log(7.4e4), 3600))
+    cell = 10.0 / 60
+    k = np.minimum(((x + 5) / cell).astype(int), 59) + 60 * np.minimum(((y + 5) / cell).astype(int), 59)
+    return eng.Catalog(t, x, y, dens[k])
+
+
+@pytest.mark.parametrize("kind", ["bench", "county"])
+def test_tr_cut_matches_exact_threshold(eng, kind):
+    """The density-scaled trigger's certified e^-46 spatial cut against the
+    flush threshold (only exact zeros dropped): LL 1e-13, gradient 1e-12, no
+    certification fallback on the BASELINE catalogs."""
+    cat = eng.benchmark_catalog(200000, 42) if kind == "bench" else county_like(eng, 200000)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant.varying)
+    ev = eng.Evaluator(cat)
+    a = ev.eval(p, grad=True)
+    assert ev.fgt_stats()[1] == 0
+    ev.set_tr_cut(False)
+    b = ev.eval(p, grad=True)
+    close(a, b)
+
+
+def test_tr_cut_certification_fallback(eng, monkeypatch):
+    cat = eng.benchmark_catalog(50000, 8)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant.varying)
+    ref = eng.Evaluator(cat)
+    for f in (ref.set_fgt, ref.set_bg_fgt, ref.set_tr_cut):
+        f(False)
+    want = ref.eval(p, grad=True)
+    monkeypatch.setenv("HK_FGT_ROW_TOL", "0")
+    ev = eng.Evaluator(cat)
+    got = ev.eval(p, grad=True)
+    assert got[0] == want[0] and np.array_equal(got[1], want[1])
+    assert ev.fgt_stats()[1] == 1
