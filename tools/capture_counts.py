@@ -42,7 +42,9 @@ def worker(n, mode):
 
 
 def kind_of(name):
-    if "fgt_" in name:  # the Hermite expansion's launches (hk_fgt.cu)
+    if "bg_fgt_" in name:  # the background's 1-D expansion (hk_fgt.cu)
+        return "bg_" + name.split("bg_fgt_", 1)[1].split("_kernel", 1)[0]
+    if "fgt_" in name:  # the trigger's Hermite expansion (hk_fgt.cu)
         base = name.split("fgt_", 1)[1].split("_kernel", 1)[0]
         return {"eval": "fgt_rows"}.get(base, "fgt_" + base)
     # pair_kernel<kVarying, kGrad, kMode, kF32, kOnly>
