@@ -171,7 +171,10 @@ struct DeviceState {
   double* h_out6 = nullptr;  // pinned
   // Hermite expansion of the homogeneous trigger (hk_fgt.cu): checkpoint
   // prefixes of this shard's row blocks and the per-evaluation buffers
-  int nck = 0, fgt_cols = 0;
+  // checkpoints: ck_off virtual ones (every kFgtCkRows columns below the
+  // shard's first prefix: a shard starting late must not sum its whole prefix
+  // in one increment) followed by nck_rows real ones (one per 4 row blocks)
+  int nck = 0, ck_off = 0, nck_rows = 0, fgt_cols = 0;
   double fgt_direct_cost = 0.0;  // trigger pairs the expansion replaces (sum over rows of P_k)
   int* ck_P = nullptr;                                   // [nck]
   double *fgt_tR = nullptr, *fgt_decay = nullptr, *fgt_dt = nullptr, *fgt_wsum = nullptr;  // [nck]
@@ -484,9 +487,13 @@ struct hk_ctx {
       static_assert(hk::kFgtRowBlock == hk::rows_per_item(false), "FGT checkpoints follow the homogeneous plan");
       const int bi = hk::rows_per_item(false);
       const int nblocks = (re - rb + bi - 1) / bi;
-      s.nck = (nblocks + hk::kFgtBlocks - 1) / hk::kFgtBlocks;
-      std::vector<int> ckp(s.nck);
-      for (int k = 0; k < s.nck; ++k) ckp[k] = lb[rb + k * hk::kFgtBlocks * bi] / hk::kBJ * hk::kBJ;
+      s.nck_rows = (nblocks + hk::kFgtBlocks - 1) / hk::kFgtBlocks;
+      std::vector<int> real(s.nck_rows), ckp;
+      for (int k = 0; k < s.nck_rows; ++k) real[k] = lb[rb + k * hk::kFgtBlocks * bi] / hk::kBJ * hk::kBJ;
+      for (int v = hk::kFgtCkRows; s.nck_rows && v < real[0]; v += hk::kFgtCkRows) ckp.push_back(v);
+      s.ck_off = static_cast<int>(ckp.size());
+      ckp.insert(ckp.end(), real.begin(), real.end());
+      s.nck = static_cast<int>(ckp.size());
       s.fgt_cols = s.nck ? ckp.back() : 0;
       s.ck_P = dmalloc<int>(s.nck);
       ck(cudaMemcpy(s.ck_P, ckp.data(), s.nck * sizeof(int), cudaMemcpyHostToDevice), "upload checkpoints");
@@ -495,7 +502,7 @@ struct hk_ctx {
       s.fgt_dt = dmalloc<double>(s.nck);
       s.fgt_wsum = dmalloc<double>(s.nck);
       s.cert_scratch = dmalloc<double>(4 * static_cast<std::size_t>((n + hk::kCertChunk - 1) / hk::kCertChunk));
-      s.fgt_perm = dmalloc<int>(static_cast<std::size_t>(s.nck) * hk::kFgtCkRows);
+      s.fgt_perm = dmalloc<int>(static_cast<std::size_t>(s.nck_rows) * hk::kFgtCkRows);
       static_assert((hk::kFgtCkRows & (hk::kFgtCkRows - 1)) == 0, "checkpoint windows are sorted bitonically");
       s.fgt_box = dmalloc<int>(s.fgt_cols);
       s.fgt_u = dmalloc<double>(s.fgt_cols);
@@ -504,7 +511,7 @@ struct hk_ctx {
       ck(cudaMallocHost(&s.h_fgt_flag, sizeof(unsigned)), "cudaMallocHost");
       s.fgt_direct_cost = 0.0;
       for (int b = 0; b < nblocks; ++b)
-        s.fgt_direct_cost += static_cast<double>(std::min(bi, re - rb - b * bi)) * ckp[b / hk::kFgtBlocks];
+        s.fgt_direct_cost += static_cast<double>(std::min(bi, re - rb - b * bi)) * real[b / hk::kFgtBlocks];
     }
     s.partial = dmalloc<double>(static_cast<std::size_t>(std::max({s.slots[0], s.slots[1], s.slots[2]})) * 5 *
                                 rows);
@@ -631,6 +638,8 @@ struct hk_ctx {
     F.x = s.x;
     F.y = s.y;
     F.nck = s.nck;
+    F.ck_off = s.ck_off;
+    F.nck_rows = s.nck_rows;
     F.P = s.ck_P;
     F.tR = s.fgt_tR;
     F.decay = s.fgt_decay;
@@ -763,7 +772,7 @@ struct hk_ctx {
     hk::FgtParams F{};
     if (use_fgt) {
       if (s.fgt_perm_loc != loc_version) {  // checkpoint rows in spatial order, once per location set
-        hk::launch_cluster(s.x, s.y, s.fgt_perm, s.rb, rows, hk::kFgtCkRows, s.nck, hk::kFgtLeaf, cx, cy,
+        hk::launch_cluster(s.x, s.y, s.fgt_perm, s.rb, rows, hk::kFgtCkRows, s.nck_rows, hk::kFgtLeaf, cx, cy,
                            half_extent, s.stream, hk::kFgtCkRows);
         s.fgt_perm_loc = loc_version;
         prof_total += 1;

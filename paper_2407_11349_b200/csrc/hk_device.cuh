@@ -37,9 +37,12 @@
 namespace hk {
 
 // Kernel shape (overridable at build time for tuning experiments).  Rows
-// per thread differ by variant (measured, tools/tune_shapes.sh): the
+// per thread (measured, tools/tune_shapes.sh, tools/tune_trig.sh): the
 // constant kernel amortises each staged column over 4 rows; the varying
-// kernel keeps 2 so its per-row-slot skip votes stay cheap.
+// kernel also uses 4 since round 2: with the certified spatial cut its
+// candidates are rare and the per-32-column box tests dominate, which 4
+// rows amortise over 128-row warp clusters (N=1e6 trigger launch 19.3 ->
+// 17.5 ms on the bench catalog, county catalog +1.5%).
 #ifndef HK_THREADS
 #define HK_THREADS 128
 #endif
@@ -47,7 +50,7 @@ namespace hk {
 #define HK_ROWS_CONST 4
 #endif
 #ifndef HK_ROWS_VAR
-#define HK_ROWS_VAR 2
+#define HK_ROWS_VAR 4
 #endif
 #ifndef HK_UNROLL
 #define HK_UNROLL 4
@@ -62,7 +65,7 @@ __host__ __device__ constexpr int rows_per_item(bool varying) {
 }
 // resident CTAs per SM the register budget is sized for (64K regs)
 #ifndef HK_MIN_BLOCKS_TRIG
-#define HK_MIN_BLOCKS_TRIG 6  // density-scaled trigger-only launches
+#define HK_MIN_BLOCKS_TRIG 4  // density-scaled trigger-only launches
 #endif
 #ifndef HK_MIN_BLOCKS_CONST
 #define HK_MIN_BLOCKS_CONST 3

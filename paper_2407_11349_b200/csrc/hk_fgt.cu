@@ -104,11 +104,15 @@ __global__ void fgt_assign_kernel(const FgtParams F) {
 // v^b/b! staged in shared memory, and each lane sums its coefficients over
 // the sources in that order.
 
-constexpr int kMomThreads = 128;
+constexpr int kMomThreads = 256;
 constexpr int kMomWarps = kMomThreads / 32;
-constexpr int kMomBatch = 32;  // sources per batch and warp (one 32-column chunk fits)
-// dynamic shared memory: per warp kMomBatch x 3P doubles (W u^a/a!, (t_R - t) W u^a/a!, v^b/b!)
-constexpr int kMomSmem = kMomWarps * kMomBatch * (3 * P) * static_cast<int>(sizeof(double));
+constexpr int kMomBatch = 16;   // sources per batch and warp
+constexpr int kMomSort = 2048;  // sources sorted by box per pass (a power of two)
+// dynamic shared memory: per warp kMomBatch x 3P doubles (W u^a/a!, (t_R - t) W u^a/a!, v^b/b!),
+// then the pass's sort keys and each box's first position
+constexpr int kMomSmem = kMomWarps * kMomBatch * (3 * P) * static_cast<int>(sizeof(double)) +
+                         kMomSort * static_cast<int>(sizeof(unsigned)) +
+                         (kFgtMaxBoxes + 1) * static_cast<int>(sizeof(int));
 
 // adds the batch's sources (in batch order) to the box's coefficients: lane
 // b (< P) owns the coefficients (a, b) of both sets for every a, so per
@@ -138,58 +142,80 @@ __device__ __forceinline__ void fgt_flush(double* ob, bool grad, int nb, const d
   }
 }
 
-constexpr int kMomBoxesPerCta = 16;  // grid: (checkpoint, group of 16 boxes)
-
+// One CTA per checkpoint interval [P_{k-1}, P_k): its sources are sorted by
+// (box, column) in shared memory (bitonic, kMomSort per pass), so every box's
+// sources are one contiguous run, summed in column order by one warp.
 __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParams F) {
   extern __shared__ __align__(16) double s_dyn[];
   const int k = blockIdx.x;
-  const int B_end = min(F.nbox, (static_cast<int>(blockIdx.y) + 1) * kMomBoxesPerCta);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* wpu = s_dyn + warp * kMomBatch * (3 * P);  // [s][2][P]
   double* pv = wpu + kMomBatch * 2 * P;              // [s][P]
+  unsigned* keys = reinterpret_cast<unsigned*>(s_dyn + kMomWarps * kMomBatch * 3 * P);
+  int* start = reinterpret_cast<int*>(keys + kMomSort);
   const int j0 = k ? F.P[k - 1] : 0, j1 = F.P[k];
   const double tR = F.tR[k];
   const bool grad = F.grad != 0;
   double* out = F.mom + static_cast<size_t>(k) * F.nbox * 2 * PP;
-  for (int B = blockIdx.y * kMomBoxesPerCta + warp; B < B_end; B += kMomWarps) {
-    double* ob = out + static_cast<size_t>(B) * 2 * PP;
-    for (int c = lane; c < (grad ? 2 : 1) * PP; c += 32) ob[c] = 0.0;
-    __syncwarp();
-    int nb = 0;
-    for (int c0 = j0; c0 < j1; c0 += 32) {
-      const int j = c0 + lane;
-      const bool in = j < j1 && F.box[j] == B;
-      const unsigned m = __ballot_sync(0xffffffffu, in);
-      const int cnt = __popc(m);
-      if (cnt == 0) continue;
-      if (nb + cnt > kMomBatch) {
+  for (int c = threadIdx.x; c < F.nbox * 2 * PP; c += kMomThreads)
+    if (grad || c % (2 * PP) < PP) out[c] = 0.0;
+  for (int p0 = j0; p0 < j1; p0 += kMomSort) {
+    const int cnt = min(kMomSort, j1 - p0);
+    __syncthreads();  // the previous pass is done with keys / start; the zero fill is visible
+    for (int i = threadIdx.x; i < kMomSort; i += kMomThreads)
+      keys[i] = i < cnt ? (static_cast<unsigned>(F.box[p0 + i]) << 12) | static_cast<unsigned>(i) : 0xffffffffu;
+    __syncthreads();
+    for (int kk = 2; kk <= kMomSort; kk <<= 1)
+      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+        for (int i = threadIdx.x; i < kMomSort; i += kMomThreads) {
+          const int l = i ^ jj;
+          if (l > i) {
+            const unsigned x = keys[i], y = keys[l];
+            if ((x > y) == ((i & kk) == 0)) {
+              keys[i] = y;
+              keys[l] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    for (int B = threadIdx.x; B <= F.nbox; B += kMomThreads) {  // first position of box B
+      int lo = 0, hi = cnt;
+      const unsigned kb = static_cast<unsigned>(B) << 12;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < kb) lo = mid + 1;
+        else hi = mid;
+      }
+      start[B] = lo;
+    }
+    __syncthreads();
+    for (int B = warp; B < F.nbox; B += kMomWarps) {
+      double* ob = out + static_cast<size_t>(B) * 2 * PP;
+      for (int s0 = start[B]; s0 < start[B + 1]; s0 += kMomBatch) {
+        const int nb = min(kMomBatch, start[B + 1] - s0);
+        if (lane < nb) {
+          const int j = p0 + static_cast<int>(keys[s0 + lane] & 0xfffu);
+          const double u = F.u[j], v = F.v[j];
+          const double dtj = tR - F.t[j];
+          const double wj = exp(-F.omega * dtj);
+          double a1 = wj, a2 = dtj * wj, b1 = 1.0;
+#pragma unroll 1
+          for (int n = 0; n < P; ++n) {
+            wpu[lane * 2 * P + n] = a1;
+            wpu[lane * 2 * P + P + n] = a2;
+            pv[lane * P + n] = b1;
+            const double f = c_recip.v[n];
+            a1 = a1 * u * f;
+            a2 = a2 * u * f;
+            b1 = b1 * v * f;
+          }
+        }
         __syncwarp();
         fgt_flush(ob, grad, nb, wpu, pv, lane);
         __syncwarp();
-        nb = 0;
       }
-      if (in) {
-        const int s = nb + __popc(m & ((1u << lane) - 1u));
-        const double u = F.u[j], v = F.v[j];
-        const double dtj = tR - F.t[j];
-        const double wj = exp(-F.omega * dtj);
-        double a1 = wj, a2 = dtj * wj, b1 = 1.0;
-#pragma unroll 1
-        for (int n = 0; n < P; ++n) {
-          wpu[s * 2 * P + n] = a1;
-          wpu[s * 2 * P + P + n] = a2;
-          pv[s * P + n] = b1;
-          const double f = c_recip.v[n];
-          a1 = a1 * u * f;
-          a2 = a2 * u * f;
-          b1 = b1 * v * f;
-        }
-      }
-      nb += cnt;
     }
-    __syncwarp();
-    if (nb) fgt_flush(ob, grad, nb, wpu, pv, lane);
-    __syncwarp();
   }
 }
 
@@ -246,7 +272,7 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 2)
   // windows = checkpoints, leaves = one warp's kFgtLeaf rows): a warp's rows
   // are close together, so boxes beyond the cut-off of all of them are skipped
   const int cta_rows = R * kFgtEvalThreads;
-  const int k = (blockIdx.x * cta_rows) / kFgtCkRows;
+  const int k = F.ck_off + (blockIdx.x * cta_rows) / kFgtCkRows;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int li[R];
   bool valid[R];
@@ -542,8 +568,7 @@ void launch_fgt_prepare(const FgtParams& F, cudaStream_t s) {
   fgt_refs_kernel<<<(F.nck + 127) / 128, 128, 0, s>>>(F);
   if (F.ncols > 0) fgt_assign_kernel<<<(F.ncols + 255) / 256, 256, 0, s>>>(F);
   cudaFuncSetAttribute(fgt_moments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMomSmem);
-  const dim3 grid(F.nck, (F.nbox + kMomBoxesPerCta - 1) / kMomBoxesPerCta);
-  fgt_moments_kernel<<<grid, kMomThreads, kMomSmem, s>>>(F);
+  fgt_moments_kernel<<<F.nck, kMomThreads, kMomSmem, s>>>(F);
   fgt_scan_kernel<<<(F.nbox * PP + 255) / 256, 256, 0, s>>>(F);
   fgt_wsum_kernel<<<(F.nck + 127) / 128, 128, 0, s>>>(F);
 }
@@ -566,7 +591,7 @@ void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* 
 void launch_fgt_eval(const FgtParams& F, int rows_base, int rows_total, const double* bg_sums,
                      double* tr_sums, double coef_a, double coef_c, unsigned* flag, cudaStream_t s) {
   const int rows_per_cta = kFgtRowsPerThread * kFgtEvalThreads;
-  const int blocks = F.nck * (kFgtCkRows / rows_per_cta);  // the permutation's positions
+  const int blocks = F.nck_rows * (kFgtCkRows / rows_per_cta);  // the permutation's positions
   if (F.grad)
     fgt_eval_kernel<true><<<blocks, kFgtEvalThreads, 0, s>>>(F, rows_base, rows_total, bg_sums, tr_sums,
                                                              coef_a, coef_c, flag);

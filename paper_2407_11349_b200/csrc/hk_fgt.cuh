@@ -9,7 +9,7 @@ constexpr int kFgtP = 30;              // Hermite terms per dimension (a, b < kF
 constexpr double kFgtGamma = 1.4142135623730951;  // box side / sqrt(delta): rho = 1
 constexpr int kFgtBlocks = 4;          // homogeneous row blocks per checkpoint
 constexpr int kFgtRowBlock = 512;      // rows per block of the homogeneous plan (rows_per_item(false))
-constexpr int kFgtEvalThreads = 128;   // threads per evaluation CTA
+constexpr int kFgtEvalThreads = 32;    // threads per evaluation CTA: one warp (no cross-warp barrier when warps skip boxes)
 constexpr int kFgtRowsPerThread = 2;   // rows per thread (kFgtEvalThreads x this divides kFgtRowBlock)
 constexpr int kFgtCkRows = kFgtBlocks * kFgtRowBlock;  // rows per checkpoint (a power of two)
 constexpr int kFgtLeaf = 32 * kFgtRowsPerThread;       // one warp's rows: a k-d leaf
@@ -20,7 +20,8 @@ constexpr int kFgtMaxBoxes = 1024;     // larger grids (small sigma_x / wide cat
 struct FgtParams {
   int n, ncols;                 // catalog size; columns below the last prefix
   const double *t, *x, *y;
-  int nck;                      // checkpoints
+  int nck;                      // checkpoints (ck_off virtual ones, then nck_rows with rows)
+  int ck_off, nck_rows;
   const int* P;                 // [nck] prefix boundaries (columns [0, P_k)), nondecreasing
   double* tR;                   // [nck] reference times t[P_k]
   double* decay;                // [nck] exp(-omega (tR_k - tR_{k-1}))
