@@ -364,9 +364,11 @@ def run_ours(args):
     # Hermite expansion off): the pure O(N^2) kernel, one evaluation
     ev.set_bg_expansion(False)
     ev.set_fgt(False)
+    ev.set_bg_fgt(False)
     d_ms, d_kinds, _, _ = timed(HawkesParams(**BENCH_PARAMS, variant=Variant.constant), 1, 1)
     ev.set_bg_expansion(True)
     ev.set_fgt(True)
+    ev.set_bg_fgt(True)
     fgt_stats = ev.fgt_stats()
 
     if rank == 0:
@@ -460,6 +462,7 @@ def run_ours(args):
                 "note": "one homogeneous LL+grad evaluation with the background block expansion and the "
                         "trigger's Hermite expansion disabled: every ordered pair evaluated directly",
                 "ms_per_step": d_ms, "pair_both_ms": d_kinds[0],
+                "note2": "both Hermite expansions and the background block expansion off",
                 "roofline": roofline(f"direct_{n}_both", d_kinds[0], fp64_peak, pairs_local,
                                      algo_bytes("constant", "both"))},
         }

@@ -185,7 +185,7 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
   // and slot) is therefore O(N) with a bounded constant: 17 slots at
   // N = 1e6 (0.68 GB), 20 at N = 1e7 (8 GB).  HK_ITEM_TARGET overrides the
   // item target (tuning).
-  int target = kItemTarget;
+  int target = G > 1 ? kItemTargetVarying : kItemTarget;
   if (const char* e = std::getenv("HK_ITEM_TARGET")) target = std::max(1, std::atoi(e));
   int slots = std::min(kMaxSlots, (target + nblocks - 1) / nblocks);
   slots = std::max(slots, (ntiles + kMaxItemTiles - 1) / kMaxItemTiles);

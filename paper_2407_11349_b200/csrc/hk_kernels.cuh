@@ -25,6 +25,10 @@ constexpr int kMaxItemTiles = 2048;  // te - tb (the pair kernel classifies them
 // the pair kernel keeps speeding up with more, smaller items up to here
 // (3552 items: 543.5 ms, 7104: 522.9, 14208: 510.1, 31264: 503.9).
 constexpr int kItemTarget = 148 * 3 * 72;
+// The density-scaled (clustered, trigger-only) plan: half as many items are
+// as fast there (N=1e6: 16000 items 17.48 ms = 31968 items; county catalog
+// +0.5%) and halve its partial-sum traffic.
+constexpr int kItemTargetVarying = 16000;
 // Column chunks per row block at most: the partial-sum buffer holds
 // slots x 40 B per row.
 constexpr int kMaxSlots = 64;

@@ -38,6 +38,7 @@ def worker(n, mode):
     if mode == "direct":
         ev.set_bg_expansion(False)
         ev.set_fgt(False)
+        ev.set_bg_fgt(False)
     ev.eval(p, grad=True)
 
 
