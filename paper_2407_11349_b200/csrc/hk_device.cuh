@@ -32,7 +32,16 @@
 //   kChecked anything else: also rejects arguments whose k left int32.
 #pragma once
 
+#include <cassert>
 #include <cstdint>
+
+// Device-side bounds checks of the debug build (make debug: -DHK_DEBUG);
+// compiled out otherwise.
+#ifdef HK_DEBUG
+#define HK_ASSERT(x) assert(x)
+#else
+#define HK_ASSERT(x) ((void)0)
+#endif
 
 namespace hk {
 

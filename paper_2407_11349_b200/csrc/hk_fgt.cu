@@ -93,6 +93,7 @@ __global__ void fgt_assign_kernel(const FgtParams F) {
   const int bx = min(max(static_cast<int>(floor((x - F.x0) / F.L)), 0), F.nb - 1);
   const int by = min(max(static_cast<int>(floor((y - F.y0) / F.L)), 0), F.nb - 1);
   F.box[j] = bx + F.nb * by;
+  HK_ASSERT(bx + F.nb * by < F.nbox && F.nbox <= kFgtMaxBoxes);
   F.u[j] = (x - (F.x0 + (bx + 0.5) * F.L)) * F.inv_sqd;
   F.v[j] = (y - (F.y0 + (by + 0.5) * F.L)) * F.inv_sqd;
 }
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParam
     __syncthreads();  // the previous pass is done with keys / start; the zero fill is visible
     for (int i = threadIdx.x; i < kMomSort; i += kMomThreads)
       keys[i] = i < cnt ? (static_cast<unsigned>(F.box[p0 + i]) << 12) | static_cast<unsigned>(i) : 0xffffffffu;
+    HK_ASSERT(j1 <= F.ncols && kMomSort <= 4096);
     __syncthreads();
     for (int kk = 2; kk <= kMomSort; kk <<= 1)
       for (int jj = kk >> 1; jj > 0; jj >>= 1) {
@@ -280,7 +282,9 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 2)
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int pos = blockIdx.x * cta_rows + warp * kFgtLeaf + r * 32 + lane;
+    HK_ASSERT(pos < F.nck_rows * kFgtCkRows && k < F.nck);
     const int row = F.perm[pos];
+    HK_ASSERT(row < 0 || (row >= rows_base && row < rows_base + rows_total));
     valid[r] = row >= 0;
     li[r] = valid[r] ? row - rows_base : 0;
     const int rr = valid[r] ? row : rows_base;
@@ -522,7 +526,8 @@ __global__ void __launch_bounds__(kBgThreads) bg_fgt_eval_kernel(const BgFgtPara
     const double d = fmax(fabs(X) - hs, 0.0);
     if (d * d > kFgtCut) continue;
     used += F.count[b];
-    const double* A = F.mom + b * P;
+    HK_ASSERT(b >= 0 && b < F.nbt);
+  const double* A = F.mom + b * P;
     const double X2 = 2.0 * X;
     double h0 = exp(-X * X), h1 = X2 * h0;
     double h2 = fma(X2, h1, -2.0 * h0);

@@ -50,13 +50,6 @@ namespace hk {
 
 namespace {
 
-// Device-side bounds checks of the debug build (make debug: -DHK_DEBUG);
-// compiled out otherwise.
-#ifdef HK_DEBUG
-#define HK_ASSERT(x) assert(x)
-#else
-#define HK_ASSERT(x) ((void)0)
-#endif
 
 enum TileType { kSkip = 0, kTileBT = 1, kTileB = 2, kTileT = 3, kTileM = 4, kTileBTx = 5, kTileBx = 6 };
 

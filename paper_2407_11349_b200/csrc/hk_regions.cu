@@ -31,6 +31,7 @@
 #include <string>
 #include <vector>
 
+#include "hk_device.cuh"
 #include "hk_regions.hpp"
 
 namespace hk {
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(kSampleThreads)
   const int k = blockIdx.x * kSampleThreads + threadIdx.x;
   if (k >= R.n_events) return;
   const int e = R.perm[k];
+  HK_ASSERT(e >= 0 && e < R.n_events);
   const int r = R.event_region[e];
   const int kind = R.kind[r];
   if (kind == kRegionPoint) {
