@@ -290,6 +290,11 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
     // spatially clustered (cluster_kernel), so the boxes are small.  Only
     // exact zeros are skipped and each row still sums in increasing j: the
     // result is bitwise that of the dense loop.
+    // unrolled over the tile's 8 chunks: the lane's staged-column address is
+    // then one base register plus immediate offsets (rolled, the compiler
+    // rematerialised it from SR_TID and the stage base for every chunk: 9 of
+    // the test's 21 instructions)
+#pragma unroll
     for (int c = 0; c < kBJ; c += 32) {
       unsigned cand = warp_candidates(R, fbuf, c);
       while (cand) {  // warp-uniform
