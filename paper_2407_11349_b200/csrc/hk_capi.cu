@@ -609,7 +609,7 @@ struct hk_ctx {
       expanded += per_row * (s.re - s.rb);
       moments = std::max(moments, static_cast<std::size_t>(s.nck) * nb * nb * 2 * hk::kFgtP * hk::kFgtP);
     }
-    if (!(expanded < 0.5 * direct) || moments * sizeof(double) > (std::size_t{6} << 30)) return f;
+    if (!(expanded < 0.5 * direct) || moments * sizeof(double) > (std::size_t{48} << 30)) return f;
     f.on = true;
     f.nb = nb;
     f.L = L;
