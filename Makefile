@@ -6,7 +6,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -v
 CSRC := paper_2407_11349_b200/csrc
 LIB := paper_2407_11349_b200/libhawkes_b200.so
-SRCS := $(CSRC)/hk_kernels.cu $(CSRC)/hk_capi.cu $(CSRC)/hk_regions.cu $(CSRC)/hk_fgt.cu $(CSRC)/hk_host.cpp
+SRCS := $(CSRC)/hk_kernels.cu $(CSRC)/hk_capi.cu $(CSRC)/hk_regions.cu $(CSRC)/hk_fgt.cu $(CSRC)/hk_cells.cu $(CSRC)/hk_host.cpp
 HDRS := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) include/hawkes_b200.h
 
 all: $(LIB) oracle

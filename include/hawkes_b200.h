@@ -225,6 +225,11 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
  *     the dropped weight is bounded per row and certified like the
  *     expansions (1e-13 relative to the row's rate, else recomputed). */
 #define HK_OPT_TR_CUT 4
+/*   HK_OPT_CELLS: the density-scaled FP64 trigger visits its sources
+ *     regrouped by spatial cell (tiles of one cell, time order within it),
+ *     so whole tiles beyond a block's reach are skipped; 0 visits them in
+ *     time order.  Same sums, different summation order. */
+#define HK_OPT_CELLS 5
 int hk_set_option(hk_ctx* ctx, int option, int value);
 /* Evaluations that used a Hermite expansion (trigger or background),
  * synchronous ones recomputed

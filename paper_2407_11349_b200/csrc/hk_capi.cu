@@ -160,8 +160,16 @@ struct DeviceState {
   // variant, see enqueue), [1] varying (clustered windows)
   // [2]: the homogeneous trigger-only plan with the Hermite expansion
   // (hk_host.cpp plan_items_fgt: one item per row block over its band)
-  hk::Item* items[3] = {nullptr, nullptr, nullptr};
-  int n_items[3] = {0, 0, 0}, slots[3] = {0, 0, 0};
+  // [3]: the density-scaled FP64 trigger over spatial cell tiles (hk_cells.cu)
+  hk::Item* items[4] = {nullptr, nullptr, nullptr, nullptr};
+  int n_items[4] = {0, 0, 0, 0}, slots[4] = {0, 0, 0, 0};
+  // spatial cell tiles (hk_cells.cu): the column regrouping of location
+  // version cells_loc, and its per-evaluation arrays
+  hk::CellGrid cgrid{};
+  hk::CellLayout cells{};
+  int *cell_id = nullptr, *cell_chunk = nullptr, *cell_start = nullptr, *cell_perm = nullptr,
+      *cell_nct = nullptr;
+  long cells_loc = -1;
   double* partial = nullptr;
   double* bg_sums[2] = {nullptr, nullptr};  // [B, B2] x rows, LRU-2 (workspace cache)
   double* tr_sums[2] = {nullptr, nullptr};  // [T, Td, Tq] x rows
@@ -226,6 +234,7 @@ struct hk_ctx {
   int fgt_enabled = 1;     // HK_OPT_FGT
   int bg_fgt_enabled = 1;  // HK_OPT_BG_FGT
   int tr_cut_enabled = 1;  // HK_OPT_TR_CUT
+  int cells_enabled = 1;   // HK_OPT_CELLS
   long fgt_evals = 0, fgt_fallbacks = 0;
   bool fgt_pending = false;  // an async evaluation's certification flag is unread
 
@@ -282,6 +291,15 @@ struct hk_ctx {
       if (s.lb) cudaFree(s.lb);
       if (s.ub) cudaFree(s.ub);
       if (s.rperm) cudaFree(s.rperm);
+      for (void* q : {static_cast<void*>(s.cell_id), static_cast<void*>(s.cell_chunk),
+                      static_cast<void*>(s.cell_start), static_cast<void*>(s.cell_perm),
+                      static_cast<void*>(s.cell_nct), static_cast<void*>(s.cells.xy),
+                      static_cast<void*>(s.cells.wk), static_cast<void*>(s.cells.vz),
+                      static_cast<void*>(s.cells.fxy), static_cast<void*>(s.cells.t),
+                      static_cast<void*>(s.cells.q), static_cast<void*>(s.cells.box),
+                      static_cast<void*>(s.cells.r2), static_cast<void*>(s.cells.tmin),
+                      static_cast<void*>(s.cells.tmax)})
+        if (q) cudaFree(q);
       for (hk::Item* it : s.items)
         if (it) cudaFree(it);
       if (s.h_out6) cudaFreeHost(s.h_out6);
@@ -474,6 +492,46 @@ struct hk_ctx {
                     cudaMemcpyHostToDevice),
          "upload items");
     }
+    if (s.window > 1) {
+      // spatial cell tiles of the density-scaled FP64 trigger: a gc x gc grid
+      // by catalog size (measured on the bench catalog, trigger ms: N=1e5
+      // gc 1/2/4 = 0.53/0.55/0.76, county 1.05/1.19/1.37; 3e5 gc 1/2/4 =
+      // 2.32/2.13/2.19; 1e6 gc 4/8/16 = 8.5/8.4/11.9; 1e7 gc 4/8/12/16 =
+      // 731/712/980/1070: cells larger than the sources' reach gain no
+      // skips, while a cell tile's time span, 256 gc^2 / n of the catalog,
+      // sets how many tiles straddle a block's rows); every cell wastes at
+      // most one partial tile
+      int gc = n < 150000 ? 1 : n < 600000 ? 2 : n < 900000 ? 4 : 8;
+      if (const char* e = std::getenv("HK_CELL_GC")) gc = std::min(64, std::max(1, std::atoi(e)));  // tuning
+      const int ncell = gc * gc;
+      const int max_tiles = (n + hk::kBJ - 1) / hk::kBJ + ncell;
+      const std::size_t npos = static_cast<std::size_t>(max_tiles) * hk::kBJ;
+      s.cgrid.gc = gc;
+      s.cell_id = dmalloc<int>(n);
+      s.cell_chunk = dmalloc<int>(static_cast<std::size_t>((n + 1023) / 1024) * ncell);
+      s.cell_start = dmalloc<int>(ncell + 1);
+      s.cell_perm = dmalloc<int>(npos);
+      s.cell_nct = dmalloc<int>(1);
+      s.cells.perm = s.cell_perm;
+      s.cells.n_ctiles = s.cell_nct;
+      s.cells.max_tiles = max_tiles;
+      s.cells.xy = dmalloc<double2>(npos);
+      s.cells.wk = dmalloc<double2>(npos);
+      s.cells.vz = dmalloc<double2>(npos);
+      s.cells.fxy = dmalloc<float4>(npos);
+      s.cells.t = dmalloc<double>(npos);
+      s.cells.q = dmalloc<double>(npos);
+      s.cells.box = dmalloc<float4>(max_tiles);
+      s.cells.r2 = dmalloc<float>(max_tiles);
+      s.cells.tmin = dmalloc<double>(max_tiles);
+      s.cells.tmax = dmalloc<double>(max_tiles);
+      std::vector<hk::Item> items;
+      s.slots[3] = hk::plan_items(lb, ub, n, rb, re, hk::rows_per_item(true), items, s.window, max_tiles);
+      s.n_items[3] = static_cast<int>(items.size());
+      s.items[3] = dmalloc<hk::Item>(items.size());
+      ck(cudaMemcpy(s.items[3], items.data(), items.size() * sizeof(hk::Item), cudaMemcpyHostToDevice),
+         "upload items");
+    }
     {
       std::vector<hk::Item> items;
       s.slots[2] = hk::plan_items_fgt(lb, ub, n, rb, re, hk::rows_per_item(false), items);
@@ -513,7 +571,7 @@ struct hk_ctx {
       for (int b = 0; b < nblocks; ++b)
         s.fgt_direct_cost += static_cast<double>(std::min(bi, re - rb - b * bi)) * real[b / hk::kFgtBlocks];
     }
-    s.partial = dmalloc<double>(static_cast<std::size_t>(std::max({s.slots[0], s.slots[1], s.slots[2]})) * 5 *
+    s.partial = dmalloc<double>(static_cast<std::size_t>(std::max({s.slots[0], s.slots[1], s.slots[2], s.slots[3]})) * 5 *
                                 rows);
     for (int k = 0; k < 2; ++k) {
       s.bg_sums[k] = dmalloc<double>(2 * rows);
@@ -672,6 +730,12 @@ struct hk_ctx {
     if (tr_cut_enabled && c.varying && !c.single_prec) c.tr_cut = 46.0 * hk::kLog2eT;
   }
 
+  // The density-scaled FP64 trigger runs over spatial cell tiles
+  // (hk_cells.cu) on devices with a clustered plan.
+  bool use_cells(const hk::EvalCoef& c) const {
+    return cells_enabled && c.varying && !c.single_prec && !devs.empty() && devs.front().window > 1;
+  }
+
   // The trigger half depends on the variant and on the precision.
   static int tr_variant(const hk::EvalCoef& c) { return c.varying + 2 * c.single_prec; }
 
@@ -681,7 +745,7 @@ struct hk_ctx {
   int plan_halves(const hk::EvalCoef& c, bool grad, bool force, int& bgi, int& tri, bool fgt = false,
                   bool bg_fgt = false) {
     const int bgx = c.bg_expansion + (bg_fgt ? 2 : 0);  // how the background half is computed
-    const int tr_how = (fgt ? 1 : 0) + (c.tr_cut > 0.0 ? 2 : 0);  // ... and the trigger half
+    const int tr_how = (fgt ? 1 : 0) + (c.tr_cut > 0.0 ? 2 : 0) + (use_cells(c) ? 4 : 0);  // ... and the trigger half
     // the background half is FP64 in both precisions, but each precision
     // keeps its own entries so a cached result is bitwise the fresh one of
     // the same precision (the launches differ between the two)
@@ -735,6 +799,17 @@ struct hk_ctx {
       s.rperm_loc = loc_version;
       prof_total += 1;
     }
+    const bool cells = use_cells(c) && s.window > 1 && (halves & hk::kHalfTr);
+    if (cells && s.cells_loc != loc_version) {  // columns regrouped by cell, once per location set
+      const double side = 2.0 * half_extent / s.cgrid.gc;
+      s.cgrid.x0 = cx - half_extent;
+      s.cgrid.y0 = cy - half_extent;
+      s.cgrid.inv_side = side > 0.0 ? 1.0 / side : 0.0;
+      hk::launch_cells(s.x, s.y, n, s.cgrid, s.cell_id, s.cell_chunk, s.cell_start, s.cell_perm,
+                       s.cells.max_tiles * hk::kBJ, s.cell_nct, s.stream);
+      s.cells_loc = loc_version;
+      prof_total += 3;
+    }
     const bool use_fgt = fgt && fgt->on && (halves & hk::kHalfTr) && s.nck > 0;
     const bool use_bgf = fgt && fgt->bg && (halves & hk::kHalfBg);
     const bool use_cut = c.tr_cut > 0.0 && (halves & hk::kHalfTr);
@@ -783,6 +858,10 @@ struct hk_ctx {
     }
     if (halves) {
       hk::launch_prep(dc, c, s.stream);
+      if (cells) {
+        hk::launch_prep_cells(dc, c, s.cells, s.stream);
+        prof_total += 1;
+      }
       const int v = c.varying ? 1 : 0;
       // the pair launch's plan: the expansion's band-only plan when it computes
       // just the homogeneous trigger next to the expansion
@@ -806,8 +885,9 @@ struct hk_ctx {
           });
         if (halves & hk::kHalfTr)
           timed_pair(s, 2, [&] {
-            hk::launch_pair(dc, c, s.items[1], s.n_items[1], s.partial, s.rb, rows, grad, hk::kHalfTr,
-                            s.stream);
+            const int pt = cells ? 3 : 1;
+            hk::launch_pair(dc, c, s.items[pt], s.n_items[pt], s.partial, s.rb, rows, grad, hk::kHalfTr,
+                            s.stream, false, cells ? &s.cells : nullptr);
           });
       } else {
         const int kind = halves == (hk::kHalfBg | hk::kHalfTr) ? 0 : (halves == hk::kHalfBg ? 1 : 2);
@@ -820,7 +900,7 @@ struct hk_ctx {
         if (halves & hk::kHalfBg)
           hk::launch_collapse(s.partial, s.slots[0], rows, s.bg_sums[bgi], nullptr, s.stream);
         if (halves & hk::kHalfTr)
-          hk::launch_collapse(s.partial, s.slots[1], rows, nullptr, s.tr_sums[tri], s.stream);
+          hk::launch_collapse(s.partial, s.slots[cells ? 3 : 1], rows, nullptr, s.tr_sums[tri], s.stream);
         prof_total += (halves == (hk::kHalfBg | hk::kHalfTr)) ? 5 : 3;
       } else {
         hk::launch_collapse(s.partial, s.slots[pv], rows,
@@ -1390,6 +1470,7 @@ int hk_set_option(hk_ctx* ctx, int option, int value) {
     else if (option == HK_OPT_BG_FGT) ctx->bg_fgt_enabled = value != 0;
     else if (option == HK_OPT_TR_CUT) ctx->tr_cut_enabled = value != 0;
     else if (option == HK_OPT_FGT) ctx->fgt_enabled = value != 0;
+    else if (option == HK_OPT_CELLS) ctx->cells_enabled = value != 0;
     else throw std::invalid_argument("hk_set_option: unknown option " + std::to_string(option));
   });
 }

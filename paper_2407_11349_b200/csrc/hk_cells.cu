@@ -1,0 +1,114 @@
+// Spatial cell tiles for the density-scaled trigger (csrc/hk_kernels.cu,
+// PairParams::cells).
+//
+// The density-scaled trigger reaches only a few hundredths of the domain
+// per source (with the certified cut), yet in time order every 256-column
+// tile holds columns from everywhere, so every warp had to test every
+// earlier column against its box.  Here the columns are regrouped by
+// spatial cell (a gc x gc grid over the locations' box), time-sorted within
+// each cell, and each cell's list padded to whole 256-column "cell tiles".
+// A cell tile then has a small spatial box and a time range, and a CTA
+// skips every tile whose box is beyond the reach of all its rows (one test
+// per tile instead of eight per warp) or whose times are all at or after its
+// rows'.  Tiles entirely earlier than the CTA's rows keep the factorised
+// temporal weight (t_ref = the tile's last time); the others evaluate the
+// guard t_j < t_i per pair.
+//
+// The order is a deterministic stable counting sort by cell (one warp per
+// 1024-column chunk ranks its columns with match_any in index order), so each
+// cell's columns keep their time order.  Recomputed once per location set.
+#include <cuda_runtime.h>
+
+#include "hk_device.cuh"
+#include "hk_kernels.cuh"
+
+namespace hk {
+
+namespace {
+
+constexpr int kRankChunk = 1024;
+
+__device__ __forceinline__ int cell_of(double x, double y, const CellGrid& g) {
+  const int cx = min(max(static_cast<int>(floor((x - g.x0) * g.inv_side)), 0), g.gc - 1);
+  const int cy = min(max(static_cast<int>(floor((y - g.y0) * g.inv_side)), 0), g.gc - 1);
+  return cx + g.gc * cy;
+}
+
+// per chunk of kRankChunk columns: the count of each cell
+__global__ void cells_count_kernel(const double* __restrict__ x, const double* __restrict__ y, int n,
+                                   CellGrid g, int* cell, int* chunk_counts) {
+  extern __shared__ int s_cnt[];
+  const int ncell = g.gc * g.gc;
+  for (int c = threadIdx.x; c < ncell; c += blockDim.x) s_cnt[c] = 0;
+  __syncthreads();
+  const int j0 = blockIdx.x * kRankChunk;
+  for (int j = j0 + threadIdx.x; j < min(n, j0 + kRankChunk); j += blockDim.x) {
+    const int c = cell_of(x[j], y[j], g);
+    cell[j] = c;
+    atomicAdd(&s_cnt[c], 1);  // integer counts: order-independent
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < ncell; c += blockDim.x)
+    chunk_counts[static_cast<size_t>(blockIdx.x) * ncell + c] = s_cnt[c];
+}
+
+// per cell: exclusive prefix over the chunks (in place), the cell's count,
+// then (one thread) the cells' first cell-tile positions
+__global__ void cells_scan_kernel(int n_chunks, int ncell, int* chunk_counts, int* cell_start, int* n_ctiles) {
+  for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
+    int acc = 0;
+    for (int k = 0; k < n_chunks; ++k) {
+      const int v = chunk_counts[static_cast<size_t>(k) * ncell + c];
+      chunk_counts[static_cast<size_t>(k) * ncell + c] = acc;
+      acc += v;
+    }
+    cell_start[c] = acc;  // the count, for now
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int pos = 0;
+    for (int c = 0; c < ncell; ++c) {
+      const int cnt = cell_start[c];
+      cell_start[c] = pos;
+      pos += (cnt + kBJ - 1) / kBJ * kBJ;  // whole cell tiles
+    }
+    cell_start[ncell] = pos;
+    *n_ctiles = pos / kBJ;
+  }
+}
+
+// one warp per chunk: stable ranks within the chunk, in index order
+__global__ void cells_rank_kernel(int n, int ncell, const int* __restrict__ cell,
+                                  const int* __restrict__ chunk_base, const int* __restrict__ cell_start,
+                                  int* perm) {
+  extern __shared__ int s_run[];
+  const int lane = threadIdx.x;
+  for (int c = lane; c < ncell; c += 32) s_run[c] = chunk_base[static_cast<size_t>(blockIdx.x) * ncell + c];
+  __syncwarp();
+  const int j0 = blockIdx.x * kRankChunk;
+  for (int s = j0; s < min(n, j0 + kRankChunk); s += 32) {
+    const int j = s + lane;
+    const bool ok = j < n;
+    const int c = ok ? cell[j] : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, c);
+    const int before = __popc(peers & ((1u << lane) - 1u));
+    if (ok) perm[cell_start[c] + s_run[c] + before] = j;
+    __syncwarp();
+    if (ok && before == 0) s_run[c] += __popc(peers);  // the group's first lane advances the cell
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+void launch_cells(const double* x, const double* y, int n, const CellGrid& g, int* cell, int* chunk_counts,
+                  int* cell_start, int* perm, int perm_len, int* n_ctiles, cudaStream_t s) {
+  const int ncell = g.gc * g.gc;
+  const int n_chunks = (n + kRankChunk - 1) / kRankChunk;
+  cudaMemsetAsync(perm, 0xff, static_cast<size_t>(perm_len) * sizeof(int), s);  // -1: padding
+  cells_count_kernel<<<n_chunks, 256, ncell * sizeof(int), s>>>(x, y, n, g, cell, chunk_counts);
+  cells_scan_kernel<<<1, 256, 0, s>>>(n_chunks, ncell, chunk_counts, cell_start, n_ctiles);
+  cells_rank_kernel<<<n_chunks, 32, ncell * sizeof(int), s>>>(n, ncell, cell, chunk_counts, cell_start, perm);
+}
+
+}  // namespace hk

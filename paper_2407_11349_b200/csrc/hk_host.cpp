@@ -172,10 +172,10 @@ std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g, 
 }
 
 int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
-               int kBI, std::vector<Item>& items, int window) {
+               int kBI, std::vector<Item>& items, int window, int cell_tiles) {
   items.clear();
   const int npad = (n + kBJ - 1) / kBJ * kBJ;
-  const int ntiles = npad / kBJ;
+  const int ntiles = cell_tiles > 0 ? cell_tiles : npad / kBJ;
   const int nblocks = (re - rb + kBI - 1) / kBI;
   const int G = std::max(1, window);
   // Column chunks per row block ("slots"): about kItemTarget work items
@@ -216,7 +216,10 @@ int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, in
     for (int c = 0; c < slots; ++c) {
       const int tb = c * per, te = std::min(ntiles, (c + 1) * per);
       double cost = 0.0;
-      for (int J = tb; J < te; ++J) {
+      // cell tiles hold columns of every time: the work of a row block grows
+      // with the columns before it (its rank in time)
+      if (cell_tiles > 0) cost = static_cast<double>(te - tb) * (r0 + kBI);
+      for (int J = tb; cell_tiles <= 0 && J < te; ++J) {
         const int j0 = J * kBJ, j1 = j0 + kBJ;
         const double alpha = background_cost(static_cast<std::size_t>(n));
         if (j1 <= lbmin) cost += alpha + kCostBeta;

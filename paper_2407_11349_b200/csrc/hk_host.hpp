@@ -72,8 +72,10 @@ std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g,
 // of window * rows_per_item rows, classified against the whole window and
 // read through the clustered order rperm[(window start - rb) + ...]
 // (Item::pos; launch_cluster with the same window).
+// cell_tiles > 0: the column space is that many spatial cell tiles
+// (hk_cells.cu) instead of the time-ordered tiles.
 int plan_items(const std::vector<int>& lb, const std::vector<int>& ub, int n, int rb, int re,
-               int rows_per_item, std::vector<Item>& items, int window = 1);
+               int rows_per_item, std::vector<Item>& items, int window = 1, int cell_tiles = 0);
 
 // The homogeneous plan when the pair kernel computes only the trigger and the
 // Hermite expansion supplies every tile below each block's checkpoint: one

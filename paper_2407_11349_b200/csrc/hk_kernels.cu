@@ -93,6 +93,8 @@ struct PairParams {
   int rows_base, rows_total;
   int halves;  // kHalfBg | kHalfTr: which row sums this launch must produce
   int fgt;     // trigger below Item::xt external (hk_fgt.cu)
+  int cells;   // the items index spatial cell tiles (hk_cells.cu, L)
+  CellLayout L;
 };
 
 struct BlockInfo {
@@ -166,14 +168,15 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
       const unsigned bytes = 2 * kPair + (m ? (kVarying ? 2 : 1) * kBytes : (kGrad ? kPair : 0u)) +
                              (kVarying ? kBJ * sizeof(float4) : 0u);
       mbar_expect_tx(bar, bytes);
-      if (kVarying) bulk_g2s(fbuf, P.d.fxy + j0, kBJ * sizeof(float4), bar);
-      bulk_g2s(buf + cXY * kBJ, P.d.xy + j0, kPair, bar);
-      bulk_g2s(buf + cWK * kBJ, P.d.wk + j0, kPair, bar);
+      const bool cl = P.cells != 0;  // cell tiles: the cell-tile arrays
+      if (kVarying) bulk_g2s(fbuf, (cl ? P.L.fxy : P.d.fxy) + j0, kBJ * sizeof(float4), bar);
+      bulk_g2s(buf + cXY * kBJ, (cl ? P.L.xy : P.d.xy) + j0, kPair, bar);
+      bulk_g2s(buf + cWK * kBJ, (cl ? P.L.wk : P.d.wk) + j0, kPair, bar);
       if (m) {
-        bulk_g2s(buf + cT * kBJ, P.d.t + j0, kBytes, bar);
-        if (kVarying) bulk_g2s(buf + cQ * kBJ, P.d.q + j0, kBytes, bar);
+        bulk_g2s(buf + cT * kBJ, (cl ? P.L.t : P.d.t) + j0, kBytes, bar);
+        if (kVarying) bulk_g2s(buf + cQ * kBJ, (cl ? P.L.q : P.d.q) + j0, kBytes, bar);
       } else if (kGrad) {
-        bulk_g2s(buf + cVZ * kBJ, P.d.vz + j0, kPair, bar);
+        bulk_g2s(buf + cVZ * kBJ, (cl ? P.L.vz : P.d.vz) + j0, kPair, bar);
       }
       return;
     }
@@ -529,6 +532,47 @@ __device__ __forceinline__ void tile_masked(RowState<NR>& R, int j0, int n,
   }
 }
 
+// Cell-tile M tiles (density-scaled trigger only): columns of one spatial
+// cell spanning the CTA's rows' times.  Only the warp's candidate columns
+// (warp_candidates) are visited; each pair gets its full exponent and the
+// reference's guard t_j < t_i (model.hpp:152) as a time comparison.
+// Columns are in time order within the tile: the chunks from the first one
+// at or after the warp's last row time (t_warp_max) on are skipped.
+template <int NR, bool kGrad, int kMode>
+__device__ __forceinline__ void tile_masked_cells(RowState<NR>& R, const double* __restrict__ buf,
+                                                  const float4* __restrict__ fbuf, const EvalCoef& c,
+                                                  double t_warp_max) {
+  const double* __restrict__ st = buf + cT * kBJ;
+  const double* __restrict__ sq = buf + cQ * kBJ;
+  const double2* __restrict__ cxy = reinterpret_cast<const double2*>(buf + cXY * kBJ);
+  const double2* __restrict__ cwk = reinterpret_cast<const double2*>(buf + cWK * kBJ);
+  const double Kw = c.Kw;
+  for (int cc = 0; cc < kBJ; cc += 32) {
+    if (st[cc] >= t_warp_max) break;  // warp-uniform
+    unsigned cand = warp_candidates(R, fbuf, cc);
+    while (cand) {  // warp-uniform
+      const int j = cc + __ffs(cand) - 1;
+      cand &= cand - 1u;
+      const double tj = st[j], qj = sq[j];
+      const double2 xy = cxy[j];
+      const double Kj = cwk[j].y;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const double td = R.t[r] - tj;
+        const double dx = R.x[r] - xy.x, dy = R.y[r] - xy.y;
+        const double d2 = fma(dx, dx, dy * dy);
+        const double e = exp2_16_arg<kMode>(fma(d2, Kj, td * Kw));
+        const double g = tj < R.t[r] ? e * qj : 0.0;  // t_j < t_i
+        R.T[r] += g;
+        if (kGrad) {
+          R.Td[r] = fma(td, g, R.Td[r]);
+          R.Tq[r] = fma(qj * d2, g, R.Tq[r]);
+        }
+      }
+    }
+  }
+}
+
 // kOnly: single-half launches as their own instantiations, the other half
 // compiled out (fewer registers, more resident CTAs).  1 = background only
 // (homogeneous plan: workspace tau refreshes and the density-scaled
@@ -626,6 +670,28 @@ __global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
     R.by0 = y0;
     R.by1 = y1;
   }
+  // cell tiles: the CTA's box (union of its warps'), for the per-tile skip
+  __shared__ float4 s_wbox[kThreads / 32];
+  __shared__ double s_wtmax[kThreads / 32];  // the warp's last valid row time
+  float4 cta_box = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (kTrOnly && !kF32 && P.cells) {
+    double tm = -__longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+    for (int r = 0; r < NR; ++r)
+      if (valid[r]) tm = fmax(tm, R.t[r]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) tm = fmax(tm, __shfl_xor_sync(0xffffffffu, tm, off));
+    if ((tid & 31) == 0) s_wtmax[tid >> 5] = tm;
+    if ((tid & 31) == 0) s_wbox[tid >> 5] = make_float4(R.bx0, R.bx1, R.by0, R.by1);
+    __syncthreads();
+    cta_box = s_wbox[0];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) {
+      const float4 b = s_wbox[w];
+      cta_box = make_float4(fminf(cta_box.x, b.x), fmaxf(cta_box.y, b.y), fminf(cta_box.z, b.z),
+                            fmaxf(cta_box.w, b.w));
+    }
+  }
   __syncthreads();
 
   // Work units: one tile, or a group of consecutive Bx (background-only,
@@ -636,7 +702,25 @@ __global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
   // Tile classes of the item, once, in parallel: low nibble = the class for
   // this launch's halves, high nibble = the full (both-halves) class.
   const int ntl = it.te - it.tb;
-  HK_ASSERT(ntl >= 0 && ntl <= kMaxItemTiles && it.te * kBJ <= P.d.npad);
+  HK_ASSERT(ntl >= 0 && ntl <= kMaxItemTiles && it.te * kBJ <= (P.cells ? P.L.max_tiles * kBJ : P.d.npad));
+  if (kTrOnly && !kF32 && P.cells) {
+    // cell tiles: skip the unused tail, tiles whose every column is at or
+    // after every row, and tiles whose box is beyond the reach (largest
+    // FP32 threshold) of the CTA's box; T if every column is earlier than
+    // every row (the factorised temporal weight), M otherwise
+    const int n_ct = *P.L.n_ctiles;
+    for (int k = tid; k < ntl; k += kThreads) {
+      const int J = it.tb + k;
+      int ty = kSkip;
+      if (J < n_ct && P.L.tmin[J] < bi.t_last) {
+        const float4 b = P.L.box[J];
+        const float ex = fmaxf(fmaxf(cta_box.x - b.y, b.x - cta_box.y), 0.f);
+        const float ey = fmaxf(fmaxf(cta_box.z - b.w, b.z - cta_box.w), 0.f);
+        if (fmaf(ex, ex, ey * ey) <= P.L.r2[J]) ty = P.L.tmax[J] < bi.t_first ? kTileT : kTileM;
+      }
+      s_cls[k] = static_cast<unsigned char>(ty | (ty << 4));
+    }
+  } else
   for (int k = tid; k < ntl; k += kThreads) {
     const int ta = tile_type_all(it.tb + k, bi, P);
     // tiles below xt (all strictly earlier than the block's rows) keep only
@@ -703,11 +787,14 @@ __global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
         tile_masked<NR, kVarying, kGrad, kMode, true, false>(R, cur.J * kBJ, P.d.n, buf, fbuf, P.c);
     } else if constexpr (kTrOnly) {  // classes restricted to T and M; compact stage layout
       if (cur.type == kTileT) {
-        const double t_ref = P.d.t[cur.J * kBJ + kBJ - 1];  // the tile's last time
+        // the tile's last time (cell tiles: its own, the column order within a cell is time order)
+        const double t_ref = (!kF32 && P.cells) ? P.L.tmax[cur.J] : P.d.t[cur.J * kBJ + kBJ - 1];
         if (kF32)
           tile_trig_f32<NR, kVarying, kMode, kC>(R, nullptr, fbuf, kwbuf, P.c, t_ref);
         else
           tile_fast<NR, kVarying, kGrad, kMode, false, true, kC>(R, buf, fbuf, P.c, t_ref);
+      } else if (!kF32 && P.cells) {
+        tile_masked_cells<NR, kGrad, kMode>(R, buf, fbuf, P.c, s_wtmax[tid >> 5]);
       } else {
         tile_masked<NR, kVarying, kGrad, kMode, false, true, kC>(R, cur.J * kBJ, P.d.n, buf, fbuf,
                                                                   P.c);
@@ -808,6 +895,95 @@ __global__ void prep_kernel(const DeviceCatalog d, const EvalCoef c) {
     d.w[j] = 0.0;
     d.v[j] = 0.0;
     d.z[j] = 0.0;
+  }
+}
+
+// One CTA per cell tile (kBJ positions): the tile's first/last time, then
+// its columns' trigger values relative to the last time (w = q exp(-omega
+// (t_ref - t_j)), exactly as prep_col does for time tiles), its FP32 box and
+// largest threshold.  Unused tiles (beyond *n_ctiles) get an empty box.
+__global__ void __launch_bounds__(kBJ) prep_cells_kernel(const DeviceCatalog d, const EvalCoef c,
+                                                        const CellLayout L) {
+  __shared__ double s_t[2][kBJ / 32];
+  __shared__ float s_f[5][kBJ / 32];
+  const int J = blockIdx.x, pos = J * kBJ + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int jc = J < *L.n_ctiles ? L.perm[pos] : -1;
+  const double kInfD = __longlong_as_double(0x7ff0000000000000LL);
+  double tmin = jc >= 0 ? d.t[jc] : kInfD, tmax = jc >= 0 ? d.t[jc] : -kInfD;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    tmin = fmin(tmin, __shfl_xor_sync(0xffffffffu, tmin, off));
+    tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+  }
+  if (lane == 0) {
+    s_t[0][warp] = tmin;
+    s_t[1][warp] = tmax;
+  }
+  __syncthreads();
+  tmin = s_t[0][0];
+  tmax = s_t[1][0];
+#pragma unroll
+  for (int w = 1; w < kBJ / 32; ++w) {
+    tmin = fmin(tmin, s_t[0][w]);
+    tmax = fmax(tmax, s_t[1][w]);
+  }
+  const float kInf = __int_as_float(0x7f800000);
+  float x0 = kInf, x1 = -kInf, y0 = kInf, y1 = -kInf, r2 = -1.f;
+  if (jc >= 0) {
+    const double q = d.q[jc];
+    const double K = -(c.half_s2 * q) * kLog2eT;
+    const double dtr = tmax - d.t[jc];
+    const double w = q * exp(-c.omega * dtr);
+    const double targ = c.tr_cut > 0.0 ? c.tr_cut : kFlushArg;
+    const double r = sqrt(targ / (-K)) + 2.0 * c.f32_err;
+    const float thrf = __double2float_ru(r * r * (1.0 + 1.0 / 262144.0));
+    const float4 f = make_float4(__double2float_rn(d.x[jc] - c.cx), __double2float_rn(d.y[jc] - c.cy), thrf, 0.f);
+    L.fxy[pos] = f;
+    L.xy[pos] = make_double2(d.x[jc], d.y[jc]);
+    L.wk[pos] = make_double2(w, K);
+    L.vz[pos] = make_double2(dtr * w, q * w);
+    L.t[pos] = d.t[jc];
+    L.q[pos] = q;
+    x0 = x1 = f.x;
+    y0 = y1 = f.y;
+    r2 = thrf;
+  } else {
+    L.fxy[pos] = make_float4(0.f, 0.f, -1.f, 0.f);
+    L.xy[pos] = make_double2(0.0, 0.0);
+    L.wk[pos] = make_double2(0.0, -1.0);
+    L.vz[pos] = make_double2(0.0, 0.0);
+    L.t[pos] = kInfD;  // never earlier than a row
+    L.q[pos] = 1.0;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    x0 = fminf(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+    x1 = fmaxf(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+    y0 = fminf(y0, __shfl_xor_sync(0xffffffffu, y0, off));
+    y1 = fmaxf(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+    r2 = fmaxf(r2, __shfl_xor_sync(0xffffffffu, r2, off));
+  }
+  if (lane == 0) {
+    s_f[0][warp] = x0;
+    s_f[1][warp] = x1;
+    s_f[2][warp] = y0;
+    s_f[3][warp] = y1;
+    s_f[4][warp] = r2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kBJ / 32; ++w) {
+      x0 = fminf(x0, s_f[0][w]);
+      x1 = fmaxf(x1, s_f[1][w]);
+      y0 = fminf(y0, s_f[2][w]);
+      y1 = fmaxf(y1, s_f[3][w]);
+      r2 = fmaxf(r2, s_f[4][w]);
+    }
+    L.box[J] = make_float4(x0, x1, y0, y1);
+    L.r2[J] = r2;
+    L.tmin[J] = tmin;
+    L.tmax[J] = tmax;
   }
 }
 
@@ -1177,6 +1353,10 @@ void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s) {
   prep_kernel<<<(d.npad + threads - 1) / threads, threads, 0, s>>>(d, c);
 }
 
+void launch_prep_cells(const DeviceCatalog& d, const EvalCoef& c, const CellLayout& L, cudaStream_t s) {
+  prep_cells_kernel<<<L.max_tiles, kBJ, 0, s>>>(d, c, L);
+}
+
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, double half_extent,
                     cudaStream_t s, int block_rows) {
@@ -1194,9 +1374,10 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
                  double* partial, int rows_base, int rows_total, bool with_grad, int halves,
-                 cudaStream_t s, bool fgt) {
+                 cudaStream_t s, bool fgt, const CellLayout* cells) {
   if (n_items <= 0) return;
-  PairParams P{d, c, items, partial, rows_base, rows_total, halves, fgt ? 1 : 0};
+  PairParams P{d, c, items, partial, rows_base, rows_total, halves, fgt ? 1 : 0, cells ? 1 : 0,
+               cells ? *cells : CellLayout{}};
   if (halves == kHalfBg && !c.varying) {  // background only, homogeneous plan (FP64 either way)
     switch ((with_grad && !c.single_prec ? 3 : 0) + c.mode) {
       case 0: launch_pair_t<false, false, kExact, false, 1>(P, n_items, s); break;

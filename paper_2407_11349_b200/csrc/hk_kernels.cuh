@@ -80,6 +80,29 @@ struct DeviceCatalog {
   double2* vz;       // prep: {v_j, z_j}  / 16-byte broadcast load per pair    [npad]
 };
 
+// Spatial cell tiles of the density-scaled trigger (hk_cells.cu): the grid
+// and, per location set, the columns regrouped by cell (time order kept
+// within a cell), each cell padded to whole kBJ-column cell tiles.
+struct CellGrid {
+  int gc;                       // cells per side
+  double x0, y0, inv_side;      // grid origin, 1 / cell side
+};
+struct CellLayout {
+  const int* perm;              // [npos] position -> column (-1: padding)
+  const int* n_ctiles;          // device: cell tiles in use
+  int max_tiles;                // allocated tiles (npos = max_tiles * kBJ)
+  // per evaluation (prep_cells_kernel), in cell-tile order
+  double2 *xy, *wk, *vz;        // {x, y}, {w, K}, {v, z}: w relative to the tile's last time
+  float4* fxy;                  // {x - cx, y - cy, thrf}
+  double *t, *q;
+  // per cell tile: FP32 box of its columns, largest thrf, first and last time
+  float4* box;
+  float* r2;
+  double *tmin, *tmax;
+};
+void launch_cells(const double* x, const double* y, int n, const CellGrid& g, int* cell, int* chunk_counts,
+                  int* cell_start, int* perm, int perm_len, int* n_ctiles, cudaStream_t s);
+
 // Row-sum halves: the background [B, B2] and the trigger [T, Td, Tq].
 constexpr int kHalfBg = 1, kHalfTr = 2;
 
@@ -89,6 +112,8 @@ void upload_exp2_table(cudaStream_t s);
 // 2^(j/n), j < n, each high word minus (j << (20 - log2 n)) (host).
 void make_exp2_table(double* out, int n);
 void launch_prep(const DeviceCatalog& d, const EvalCoef& c, cudaStream_t s);
+// The cell-tile arrays of this evaluation (after launch_prep's coefficients).
+void launch_prep_cells(const DeviceCatalog& d, const EvalCoef& c, const CellLayout& L, cudaStream_t s);
 // Spatially clusters the rows [rows_base, rows_base + rows) window by window
 // (k-d median splits down to `leaf` rows) into rperm, `window` (a power of
 // two) slots per window; slots without a row hold -1.  The nblocks row blocks
@@ -114,9 +139,10 @@ __host__ __device__ inline int window_of_block(int b, int nblocks, int n_windows
 }
 // fgt: the trigger of each item's tiles below Item::xt is left out (it is
 // added by the Hermite expansion, hk_fgt.cu); homogeneous plan only.
+// cells (density-scaled FP64 trigger-only launches): items index cell tiles.
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
                  double* partial, int rows_base, int rows_total, bool with_grad, int halves,
-                 cudaStream_t s, bool fgt = false);
+                 cudaStream_t s, bool fgt = false, const CellLayout* cells = nullptr);
 // Sums the partial slots per row (fixed order) into the background plane
 // pair [B, B2] and/or the trigger planes [T, Td, Tq] (either may be null).
 void launch_collapse(const double* partial, int slots, int rows_total, double* bg_sums,

@@ -301,6 +301,10 @@ class Evaluator:
         """HK_OPT_TR_CUT: the density-scaled trigger's certified e^-46 spatial cut (default on)."""
         check(lib.hk_set_option(self._h, _lib.HK_OPT_TR_CUT, int(on)))
 
+    def set_cells(self, on: bool) -> None:
+        """HK_OPT_CELLS: the density-scaled trigger over spatial cell tiles (default on)."""
+        check(lib.hk_set_option(self._h, _lib.HK_OPT_CELLS, int(on)))
+
     def fgt_stats(self):
         """(evaluations through the expansion, direct recomputations, last
         async evaluation flagged)."""

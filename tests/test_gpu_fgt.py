@@ -249,3 +249,44 @@ def test_tr_cut_certification_fallback(eng, monkeypatch):
     got = ev.eval(p, grad=True)
     assert got[0] == want[0] and np.array_equal(got[1], want[1])
     assert ev.fgt_stats()[1] == 1
+
+
+@pytest.mark.parametrize("gc", [None, "1", "3", "8"])
+@pytest.mark.parametrize("kind", ["bench", "county"])
+def test_cells_match_time_order(eng, monkeypatch, kind, gc):
+    """The density-scaled FP64 trigger over spatial cell tiles (hk_cells.cu,
+    HK_OPT_CELLS) against the time-ordered tiles: the same pairs in another
+    summation order, LL 1e-13, gradient 1e-12, for the default grid and
+    forced ones (one cell; a grid that is not a power of two; 8 x 8 on a
+    small catalog: many partial tiles)."""
+    if gc is not None:
+        monkeypatch.setenv("HK_CELL_GC", gc)
+    cat = eng.benchmark_catalog(120000, 5) if kind == "bench" else county_like(eng, 120000, seed=4)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant.varying)
+    ev = eng.Evaluator(cat)
+    a = ev.eval(p, grad=True)
+    ev.set_cells(False)
+    b = ev.eval(p, grad=True)
+    close(a, b)
+    ev.set_cells(True)  # the cache keys the layout: back to bitwise the first result
+    c = ev.eval(p, grad=True)
+    assert c[0] == a[0] and np.array_equal(c[1], a[1])
+
+
+def test_cells_degenerate_and_clustered(eng, monkeypatch):
+    """Every event at one location (an empty grid box: one cell holds all),
+    and a catalog whose events sit on a few points with tied times."""
+    monkeypatch.setenv("HK_CELL_GC", "8")
+    rng = np.random.default_rng(11)
+    n = 40000
+    t = np.sort(rng.uniform(0, 2000, n))
+    t[1000:1010] = t[1000]
+    pts = rng.uniform(-5, 5, (7, 2))
+    k = rng.integers(0, 7, n)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant.varying)
+    for cat in (eng.Catalog(t, np.zeros(n), np.zeros(n), np.full(n, 3.0)),
+                eng.Catalog(t, pts[k, 0], pts[k, 1], np.exp(rng.uniform(0, 8, n)))):
+        ev = eng.Evaluator(cat)
+        a = ev.eval(p, grad=True)
+        ev.set_cells(False)
+        close(a, ev.eval(p, grad=True))

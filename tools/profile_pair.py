@@ -34,6 +34,8 @@ evals = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 county = len(sys.argv) > 4 and sys.argv[4] == "county"
 cat = county_catalog(n) if county else benchmark_catalog(n, 42)
 ev = Evaluator(cat)
+if os.environ.get("HK_CELLS") is not None:  # HK_OPT_CELLS on/off (comparisons)
+    ev.set_cells(os.environ["HK_CELLS"] != "0")
 p = HawkesParams(mu0=1.0, tau_t=5.0, xi0=0.5, sigma_x=0.5, sigma_t=2.0, area=100.0, variant=Variant(variant))
 ev.eval(p, grad=True)
 ev.set_profiling(True)

@@ -11,7 +11,7 @@ if [ "${RUN:-0}" != 1 ]; then
     IFS=: read name rv mb <<< "$spec"
     nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC -Xptxas -v \
       -DHK_ROWS_VAR=$rv -DHK_MIN_BLOCKS_TRIG=$mb -shared $CSRC/hk_kernels.cu $CSRC/hk_capi.cu \
-      $CSRC/hk_regions.cu $CSRC/hk_fgt.cu $CSRC/hk_host.cpp -o build/tune/lib_$name.so \
+      $CSRC/hk_regions.cu $CSRC/hk_fgt.cu $CSRC/hk_cells.cu $CSRC/hk_host.cpp -o build/tune/lib_$name.so \
       2> build/tune/ptxas_$name.log &
   done
   wait
