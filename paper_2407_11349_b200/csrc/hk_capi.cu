@@ -711,6 +711,16 @@ struct hk_ctx {
     F.omega = c.omega;
     F.delta = f.delta;
     F.eps = f.eps;
+    {  // per-box truncation: every box within the full square's bound (F.eps covers it)
+      struct Table {
+        unsigned short pn[hk::kFgtR2Buckets];
+        Table() { hk::fgt_truncation_table(hk::kFgtGamma, hk::fgt_truncation_bound(hk::kFgtP, hk::kFgtGamma), pn); }
+      };
+      static const Table table;
+      std::memcpy(F.pn, table.pn, sizeof(F.pn));
+      if (std::getenv("HK_FGT_FULL_SQUARE"))  // comparisons: the full kFgtP x kFgtP square everywhere
+        for (auto& v : F.pn) v = static_cast<unsigned short>(hk::kFgtP | (hk::kFgtP << 5) | ((hk::kFgtP / 2) << 10));
+    }
     F.row_tol = hk::kFgtRowTol;
     if (const char* e = std::getenv("HK_FGT_ROW_TOL")) F.row_tol = std::atof(e);  // tests: force the fallback
     F.grad = grad ? 1 : 0;

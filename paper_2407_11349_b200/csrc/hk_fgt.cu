@@ -23,7 +23,14 @@
 // max|u| = gamma / sqrt(2) and Cramer's bound |h_n(s)| <= K 2^{n/2} sqrt(n!)
 // (K < 1.0865), the dropped terms are below
 //   eps_p = 2 K^2 C(rho) rho^p / sqrt(p!) / (1 - rho / sqrt(p+1))
-// per unit of box weight (gamma = sqrt 2, p = 30: 6.1e-16).  Boxes whose
+// per unit of box weight (gamma = sqrt 2, p = 30: 6.1e-16).  The same bound
+// carries a factor e^{-r^2/2} for a row at scaled distance r from the box
+// centre (Cramer: |h_n(s)| <= K 2^{n/2} sqrt(n!) e^{-s^2/2}, in both
+// dimensions), so a farther box needs fewer terms: per warp and box the
+// evaluation keeps two rectangles {a < a1, b < p} u {a1 <= a < p, b < b2}
+// (each a rolled loop over a with a fully unrolled b loop) with the fewest
+// terms whose dropped terms, summed exactly (fgt_truncation_table), stay
+// below eps_30 at the warp's nearest row (every box within eps_30).  Boxes whose
 // nearest point is more than sqrt(kFgtCut) scaled units from the row are
 // skipped (weight factor <= e^{-46}).  Both bounds, per row, are compared
 // with the row's rate S_i after the sum: a row whose certified error could
@@ -42,6 +49,7 @@
 // deterministic.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -257,12 +265,103 @@ __device__ __forceinline__ void hermite(double s, double (&h)[P + 2]) {
   for (int n = 1; n < P + 1; ++n) h[n + 1] = fma(2.0 * s, h[n], -2.0 * n * h[n - 1]);
 }
 
+// sA += sum_{b < 2 NP} A_ab h_b (and the gradient chains) for the
+// kFgtRowsPerThread rows: NP pairs of b, fully unrolled.
+template <int NP, bool kGrad>
+__device__ __forceinline__ void row_pairs(const double* __restrict__ Ar, const double (&hy)[kFgtRowsPerThread][P + 2],
+                                          double (&sA)[kFgtRowsPerThread], double (&sA2)[kFgtRowsPerThread],
+                                          double (&sB)[kFgtRowsPerThread]) {
+  static_assert(2 * NP <= P, "pairs of b below P");
+  constexpr int R = kFgtRowsPerThread;
+#pragma unroll
+  for (int b = 0; b < 2 * NP; b += 2) {
+    const double2 ab = *reinterpret_cast<const double2*>(Ar + b);
+    double2 bb;
+    if (kGrad) bb = *reinterpret_cast<const double2*>(Ar + PP + b);
+    // the b terms of every chain first, then the b+1 terms: each
+    // accumulator's dependent multiply-adds are 2 R (grad: 3 R) - 1
+    // independent ones apart (the DFMA latency is hidden in-thread)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      sA[r] = fma(ab.x, hy[r][b], sA[r]);
+      if (kGrad) {
+        sA2[r] = fma(ab.x, hy[r][b + 2], sA2[r]);
+        sB[r] = fma(bb.x, hy[r][b], sB[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      sA[r] = fma(ab.y, hy[r][b + 1], sA[r]);
+      if (kGrad) {
+        sA2[r] = fma(ab.y, hy[r][b + 3], sA2[r]);
+        sB[r] = fma(bb.y, hy[r][b + 1], sB[r]);
+      }
+    }
+  }
+}
+
+// Moment rows [a0, a_end) over b < 2 NP: t0 += sum_a h_a(X) S_a, S_a =
+// sum_b A_ab h_b(Y), and the gradient sums; h_a by the running three-term
+// recurrence (ha = h_a, ha1 = h_{a+1}, ha2 = h_{a+2} on entry and exit).
+template <int NP, bool kGrad>
+__device__ __forceinline__ void rect_rows(const double* __restrict__ A, int a0, int a_end,
+                                          const double (&hy)[kFgtRowsPerThread][P + 2],
+                                          const double (&X2)[kFgtRowsPerThread], double (&ha)[kFgtRowsPerThread],
+                                          double (&ha1)[kFgtRowsPerThread], double (&ha2)[kFgtRowsPerThread],
+                                          double (&t0)[kFgtRowsPerThread], double (&q1)[kFgtRowsPerThread],
+                                          double (&q2)[kFgtRowsPerThread], double (&b0)[kFgtRowsPerThread]) {
+  constexpr int R = kFgtRowsPerThread;
+#pragma unroll 1
+  for (int a = a0; a < a_end; ++a) {
+    double sA[R], sA2[R], sB[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) sA[r] = sA2[r] = sB[r] = 0.0;
+    row_pairs<NP, kGrad>(A + a * P, hy, sA, sA2, sB);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      t0[r] = fma(ha[r], sA[r], t0[r]);
+      if (kGrad) {
+        q1[r] = fma(ha2[r], sA[r], q1[r]);
+        q2[r] = fma(ha[r], sA2[r], q2[r]);
+        b0[r] = fma(ha[r], sB[r], b0[r]);
+      }
+      const double ha3 = fma(X2[r], ha2[r], -2.0 * (a + 2) * ha1[r]);  // h_{a+3}
+      ha[r] = ha1[r];
+      ha1[r] = ha2[r];
+      ha2[r] = ha3;
+    }
+  }
+}
+
+// rect_rows for a run-time pair count (warp-uniform; once per rectangle)
+template <bool kGrad>
+__device__ __forceinline__ void rect_dispatch(int np, const double* __restrict__ A, int a0, int a_end,
+                                              const double (&hy)[kFgtRowsPerThread][P + 2],
+                                              const double (&X2)[kFgtRowsPerThread], double (&ha)[kFgtRowsPerThread],
+                                              double (&ha1)[kFgtRowsPerThread], double (&ha2)[kFgtRowsPerThread],
+                                              double (&t0)[kFgtRowsPerThread], double (&q1)[kFgtRowsPerThread],
+                                              double (&q2)[kFgtRowsPerThread], double (&b0)[kFgtRowsPerThread]) {
+  if (a0 >= a_end) return;
+  static_assert(P == 30, "the cases below cover 15 pairs");
+  switch (np) {
+#define HK_FGT_CASE(k) \
+  case k:              \
+    rect_rows<k, kGrad>(A, a0, a_end, hy, X2, ha, ha1, ha2, t0, q1, q2, b0); \
+    break;
+    HK_FGT_CASE(1) HK_FGT_CASE(2) HK_FGT_CASE(3) HK_FGT_CASE(4) HK_FGT_CASE(5)
+    HK_FGT_CASE(6) HK_FGT_CASE(7) HK_FGT_CASE(8) HK_FGT_CASE(9) HK_FGT_CASE(10)
+    HK_FGT_CASE(11) HK_FGT_CASE(12) HK_FGT_CASE(13) HK_FGT_CASE(14) HK_FGT_CASE(15)
+#undef HK_FGT_CASE
+    default: break;
+  }
+}
+
 // kFgtRowsPerThread rows per thread (rows li and li + kFgtEvalThreads of the
 // CTA's 2 x kFgtEvalThreads rows): every moment pair read from shared memory
 // feeds both rows' multiply-adds (half the loads per FMA, twice the
 // independent accumulation chains per warp).
 template <bool kGrad>
-__global__ void __launch_bounds__(kFgtEvalThreads, 2)
+__global__ void __launch_bounds__(kFgtEvalThreads, kFgtEvalMinBlocks)
     fgt_eval_kernel(const FgtParams F, int rows_base, int rows_total, const double* __restrict__ bg_sums,
                     double* __restrict__ tr_sums, double coef_a, double coef_c, unsigned* flag) {
   constexpr int R = kFgtRowsPerThread;
@@ -333,6 +432,18 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 2)
         any_use = any_use || use[r];
       }
       if (__any_sync(0xffffffffu, any_use)) {
+        // the truncation for the warp's nearest row that uses the box
+        double r2m = 1e300;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (use[r]) r2m = fmin(r2m, fma(X[r], X[r], Y[r] * Y[r]));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) r2m = fmin(r2m, __shfl_xor_sync(0xffffffffu, r2m, off));
+        const int kb = static_cast<int>(fmin(r2m * (1.0 / kFgtR2Step), kFgtR2Buckets - 1.0));
+        const unsigned pn = F.pn[kb];
+        const int p = static_cast<int>(pn & 31u), a1 = static_cast<int>((pn >> 5) & 31u),
+                  np2 = static_cast<int>(pn >> 10);
+        HK_ASSERT(p >= 1 && p <= P && a1 <= p && np2 >= 1 && np2 <= (p + 1) / 2);
         // h_b(Y) for every b (register arrays, static indices); h_a(X) by the
         // running three-term recurrence inside the a loop (the loop stays
         // rolled: a fully unrolled P x P body overflows the instruction cache)
@@ -348,51 +459,10 @@ __global__ void __launch_bounds__(kFgtEvalThreads, 2)
           ha2[r] = fma(X2[r], ha1[r], -2.0 * ha[r]);
           t0[r] = q1[r] = q2[r] = b0[r] = 0.0;
         }
-#pragma unroll 1
-        for (int a = 0; a < P; ++a) {
-          const double* Ar = A + a * P;
-          double sA[R], sA2[R], sB[R];
-#pragma unroll
-          for (int r = 0; r < R; ++r) sA[r] = sA2[r] = sB[r] = 0.0;
-#pragma unroll
-          for (int b = 0; b < P; b += 2) {
-            const double2 ab = *reinterpret_cast<const double2*>(Ar + b);
-            double2 bb;
-            if (kGrad) bb = *reinterpret_cast<const double2*>(Ar + PP + b);
-            // the b terms of every chain first, then the b+1 terms: each
-            // accumulator's dependent multiply-adds are 2 R (grad: 3 R) - 1
-            // independent ones apart (the DFMA latency is hidden in-thread)
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              sA[r] = fma(ab.x, hy[r][b], sA[r]);
-              if (kGrad) {
-                sA2[r] = fma(ab.x, hy[r][b + 2], sA2[r]);
-                sB[r] = fma(bb.x, hy[r][b], sB[r]);
-              }
-            }
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              sA[r] = fma(ab.y, hy[r][b + 1], sA[r]);
-              if (kGrad) {
-                sA2[r] = fma(ab.y, hy[r][b + 3], sA2[r]);
-                sB[r] = fma(bb.y, hy[r][b + 1], sB[r]);
-              }
-            }
-          }
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            t0[r] = fma(ha[r], sA[r], t0[r]);
-            if (kGrad) {
-              q1[r] = fma(ha2[r], sA[r], q1[r]);
-              q2[r] = fma(ha[r], sA2[r], q2[r]);
-              b0[r] = fma(ha[r], sB[r], b0[r]);
-            }
-            const double ha3 = fma(X2[r], ha2[r], -2.0 * (a + 2) * ha1[r]);  // h_{a+3}
-            ha[r] = ha1[r];
-            ha1[r] = ha2[r];
-            ha2[r] = ha3;
-          }
-        }
+        // rows a < a1 over b < p, rows a1 <= a < p over b < 2 np2 (pairs
+        // of b; with p odd the extra column b = p only shrinks the bound)
+        rect_dispatch<kGrad>((p + 1) >> 1, A, 0, a1, hy, X2, ha, ha1, ha2, t0, q1, q2, b0);
+        rect_dispatch<kGrad>(np2, A, a1, p, hy, X2, ha, ha1, ha2, t0, q1, q2, b0);
 #pragma unroll
         for (int r = 0; r < R; ++r)
           if (use[r]) {
@@ -567,6 +637,49 @@ double fgt_truncation_bound(int p, double gamma) {
   double tail = 1.0;  // rho^p / sqrt(p!)
   for (int n = 1; n <= p; ++n) tail *= rho / std::sqrt(static_cast<double>(n));
   return 2.0 * K2 * C * tail / (1.0 - rho / std::sqrt(p + 1.0));
+}
+
+void fgt_truncation_table(double gamma, double target, unsigned short* pn) {
+  // term(a, b) = K^2 rho^{a+b} / sqrt(a! b!) = K^2 e_a e_b: the bound of the
+  // (a, b) term per unit weight at r = 0 (hk_fgt.cu header).  The kept set
+  // {a < a1, b < p} u {a1 <= a < p, b < b2} (b2 = 2 np2, or p) drops
+  //   out(p) = the terms with a >= p or b >= p
+  //   + (sum_{a1 <= a < p} e_a) (sum_{b2 <= b < p} e_b) K^2,
+  // every sum of positive terms taken from suffix sums (no cancellation;
+  // beyond kM the terms are below 1e-100).
+  constexpr int kM = 160;
+  const double K2 = 1.0865 * 1.0865;
+  const double rho = gamma / std::sqrt(2.0);
+  double e[kM], tail[kM + 1];
+  for (int a = 0; a < kM; ++a) e[a] = std::exp(a * std::log(rho) - 0.5 * std::lgamma(a + 1.0));
+  tail[kM] = 0.0;
+  for (int a = kM - 1; a >= 0; --a) tail[a] = tail[a + 1] + e[a];  // sum_{b >= a}
+  const double C = tail[0];
+  static_assert(kFgtP < 32 && kFgtP / 2 < 64, "p, a1 and np2 are packed in 5 + 5 + 6 bits");
+  for (int k = 0; k < kFgtR2Buckets; ++k) {
+    const double allowed = target * std::exp(0.5 * k * kFgtR2Step);  // rows at r^2 >= k step
+    int best = 1 << 30;
+    unsigned short code = static_cast<unsigned short>(kFgtP | (kFgtP << 5) | ((kFgtP / 2) << 10));  // the full square
+    for (int p = 1; p <= kFgtP; ++p) {
+      const double out = K2 * (C * tail[p] + (C - tail[p]) * tail[p]);
+      if (out > allowed) continue;
+      const int np1 = (p + 1) / 2;
+      for (int a1 = 0; a1 <= p; ++a1) {
+        const double rows = tail[a1] - tail[p];  // sum_{a1 <= a < p} e_a
+        for (int np2 = 1; np2 <= np1; ++np2) {
+          const int b2 = std::min(2 * np2, p);
+          if (out + K2 * rows * (tail[b2] - tail[p]) > allowed) continue;
+          const int cost = a1 * np1 + (p - a1) * np2;  // pairs of b
+          if (cost < best) {
+            best = cost;
+            code = static_cast<unsigned short>(p | (a1 << 5) | (np2 << 10));
+          }
+          break;  // larger np2: more pairs
+        }
+      }
+    }
+    pn[k] = code;
+  }
 }
 
 void launch_fgt_prepare(const FgtParams& F, cudaStream_t s) {

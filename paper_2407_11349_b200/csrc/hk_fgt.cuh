@@ -9,13 +9,28 @@ constexpr int kFgtP = 30;              // Hermite terms per dimension (a, b < kF
 constexpr double kFgtGamma = 1.4142135623730951;  // box side / sqrt(delta): rho = 1
 constexpr int kFgtBlocks = 4;          // homogeneous row blocks per checkpoint
 constexpr int kFgtRowBlock = 512;      // rows per block of the homogeneous plan (rows_per_item(false))
-constexpr int kFgtEvalThreads = 32;    // threads per evaluation CTA: one warp (no cross-warp barrier when warps skip boxes)
-constexpr int kFgtRowsPerThread = 2;   // rows per thread (kFgtEvalThreads x this divides kFgtRowBlock)
+#ifndef HK_FGT_THREADS
+#define HK_FGT_THREADS 64
+#endif
+#ifndef HK_FGT_MINB
+#define HK_FGT_MINB 6
+#endif
+constexpr int kFgtEvalThreads = HK_FGT_THREADS;  // threads per evaluation CTA (the warps share the staged moments)
+constexpr int kFgtEvalMinBlocks = HK_FGT_MINB;   // __launch_bounds__ minimum resident CTAs per SM
+#ifndef HK_FGT_RPT
+#define HK_FGT_RPT 1
+#endif
+constexpr int kFgtRowsPerThread = HK_FGT_RPT;  // rows per thread (kFgtEvalThreads x this divides kFgtRowBlock)
 constexpr int kFgtCkRows = kFgtBlocks * kFgtRowBlock;  // rows per checkpoint (a power of two)
 constexpr int kFgtLeaf = 32 * kFgtRowsPerThread;       // one warp's rows: a k-d leaf
 constexpr double kFgtCut = 36.0;       // boxes farther than 6 scaled units are skipped (<= e^-36 per unit weight)
 constexpr double kFgtRowTol = 1e-13;   // certified per-row relative error bound, else recompute directly
 constexpr int kFgtMaxBoxes = 1024;     // larger grids (small sigma_x / wide catalogs): direct path
+// Per (warp, box) truncation by the distance of the warp's nearest row from
+// the box centre: buckets of r^2 (scaled units) -> the kept set {a < a1,
+// b < p} u {a1 <= a < p, b < 2 np2} (fgt_truncation_table)
+constexpr int kFgtR2Buckets = 256;
+constexpr double kFgtR2Step = 0.25;
 
 struct FgtParams {
   int n, ncols;                 // catalog size; columns below the last prefix
@@ -37,6 +52,7 @@ struct FgtParams {
   double* mom;                  // [nck][nbox][2][kFgtP^2]: A (and B) moments
   double* wsum;                 // [nck] total prefix weight (sum over boxes of A_00)
   const int* perm;              // [nck * kFgtCkRows] each checkpoint's rows in spatial (k-d) order, -1: none
+  unsigned short pn[kFgtR2Buckets];  // per r^2 bucket: p | a1 << 5 | np2 << 10
 };
 
 // The background's 1-D expansion in time (hk_fgt.cu, both variants).
@@ -59,6 +75,11 @@ void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* 
 
 // eps_p of hk_fgt.cu for p terms and box side gamma sqrt(delta).
 double fgt_truncation_bound(int p, double gamma);
+// Per r^2 bucket k (r^2 >= k kFgtR2Step): the kept set {a < a1, b < p} u
+// {a1 <= a < p, b < 2 np2}, p <= kFgtP, with the fewest multiply-adds whose
+// dropped terms are bounded by `target` per unit of box weight for every row
+// at least sqrt(k kFgtR2Step) from the box centre.
+void fgt_truncation_table(double gamma, double target, unsigned short* pn);
 // reference times, box assignment, increment moments and their scan.
 void launch_fgt_prepare(const FgtParams& F, cudaStream_t s);
 // adds the expansion's trigger sums into tr_sums (planes T, Td, Tq of

@@ -290,3 +290,21 @@ def test_cells_degenerate_and_clustered(eng, monkeypatch):
         a = ev.eval(p, grad=True)
         ev.set_cells(False)
         close(a, ev.eval(p, grad=True))
+
+
+@pytest.mark.parametrize("n", [100000, 300000])
+def test_fgt_adaptive_truncation_matches_full_square(eng, monkeypatch, n):
+    """The per-box truncation (two rectangles chosen by the warp's nearest
+    row, hk_fgt.cu fgt_truncation_table) against the full 30 x 30 square
+    everywhere (HK_FGT_FULL_SQUARE): both within the same certified bound,
+    LL 1e-13, gradient 1e-12."""
+    cat = eng.benchmark_catalog(n, 17)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant.constant)
+    ev = eng.Evaluator(cat)
+    a = ev.eval(p, grad=True)
+    assert ev.fgt_stats() == (1, 0, 0)
+    monkeypatch.setenv("HK_FGT_FULL_SQUARE", "1")
+    full = eng.Evaluator(cat)
+    b = full.eval(p, grad=True)
+    assert full.fgt_stats()[:2] == (1, 0)
+    close(a, b)
