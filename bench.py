@@ -192,9 +192,17 @@ class ClockSampler:
 COUNTS = ROOT / "profiles" / "r02_fp64_counts.json"
 
 
-def lib_sha():
+def source_sha():
+    """Hash of the library's sources and build recipe: the counts below are a
+    property of the build (nvcc's output is not bit-reproducible, so the
+    binary's own hash would change on every rebuild of the same sources)."""
     import hashlib
-    return hashlib.sha256((ROOT / "paper_2407_11349_b200" / "libhawkes_b200.so").read_bytes()).hexdigest()[:16]
+    h = hashlib.sha256()
+    csrc = ROOT / "paper_2407_11349_b200" / "csrc"
+    for f in sorted(p for p in csrc.iterdir() if p.suffix in (".cu", ".cuh", ".cpp", ".hpp")) + [ROOT / "Makefile"]:
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
 
 
 def measured_counts(tag):
@@ -208,7 +216,7 @@ def measured_counts(tag):
     c = d.get("launches", {}).get(tag)
     if c is None:
         return None
-    return dict(c, stale=d.get("lib_sha16") != lib_sha(), source=str(COUNTS.relative_to(ROOT)))
+    return dict(c, stale=d.get("src_sha16") != source_sha(), source=str(COUNTS.relative_to(ROOT)))
 
 
 def roofline(tag, launch_ms, fp64_peak, pairs, algorithmic_bytes):

@@ -153,7 +153,7 @@ __device__ __forceinline__ void issue_tile(int type, int J, int cnt, double* buf
                                            float2* kwbuf, uint64_t* bar, const PairParams& P) {
   const int j0 = J * kBJ;
   constexpr unsigned kBytes = kBJ * sizeof(double);
-  HK_ASSERT(J >= 0 && cnt >= 1 && cnt <= kSlots && (J + cnt) * kBJ <= P.d.npad);
+  HK_ASSERT(J >= 0 && cnt >= 1 && cnt <= kSlots && (J + cnt) * kBJ <= (P.cells ? P.L.max_tiles * kBJ : P.d.npad));
   HK_ASSERT(type == kTileBx || cnt == 1);
   if (type == kTileBx) {  // a group of cnt background-only tiles: their times, contiguous
     mbar_expect_tx(bar, kBytes * cnt);

@@ -14,7 +14,6 @@ Workloads (benchmark_catalog(N, 42), bench params, LL + gradient):
             Hermite expansion off (the pure O(N^2) pair kernel)
 """
 import csv
-import hashlib
 import json
 import os
 import subprocess
@@ -59,8 +58,9 @@ def main():
         worker(int(sys.argv[2]), sys.argv[3])
         return
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
-    out = {"lib_sha16": hashlib.sha256((ROOT / "paper_2407_11349_b200" / "libhawkes_b200.so").read_bytes())
-           .hexdigest()[:16], "metrics": METRICS, "launches": {}}
+    sys.path.insert(0, str(ROOT))
+    from bench import source_sha  # noqa: E402
+    out = {"src_sha16": source_sha(), "metrics": METRICS, "launches": {}}
     log = ROOT / "gpurun_out"
     log.mkdir(exist_ok=True)
     for mode in ("constant", "varying", "direct"):
