@@ -993,69 +993,155 @@ __global__ void __launch_bounds__(kBJ) prep_cells_kernel(const DeviceCatalog d, 
 constexpr int kClusterThreads = 1024;
 // kMaxClusterWindow (hk_kernels.cuh) rows per window at most
 
-// k-d median splits by sorting: the window is sorted by x, each half by y,
-// each quarter by x, ... down to `leaf` rows (one warp's rows).  Keys are the
-// FP32 coordinates quantised to 16 bits over the locations' bounding box
-// (the splits only need approximate medians) and rows a 16-bit index within
-// the window: 6 bytes per row, so a 32768-row window fits in 192 KB.  Every
-// segment ends ascending, so the padding entries (keys and index 0xffff)
-// end up at the window's tail at every level.
+// k-d median splits: the window's rows are split at the median x, each half
+// at its median y, each quarter at its median x, ... down to `leaf` rows (one
+// warp's rows).  The window is sorted ONCE by x and once by y (bitonic sorts
+// of 32-bit keys: the FP32 coordinate quantised to 16 bits over the
+// locations' bounding box, then a 16-bit index within the window, so the
+// order is total and deterministic); every level then splits the list sorted
+// along its axis at the segment midpoints and stably partitions the other
+// list by that membership (a bit per row, a block-wide scan of 32-position
+// words), so both lists stay sorted within the new segments.  O(n) per level
+// instead of a sort per level.  Padding slots (window_rows <= i < window)
+// carry the largest keys on both axes, so they end at the window's tail.
 __device__ __forceinline__ unsigned quantise16(double v, double c, double inv_extent) {
   const double q = (v - c) * inv_extent * 32767.0 + 32767.5;  // [-extent, extent] -> [0, 65535)
   return static_cast<unsigned>(fmin(fmax(q, 0.0), 65534.0));
+}
+
+__device__ __forceinline__ void bitonic_sort_u32(unsigned* a, int n) {
+  for (int k = 2; k <= n; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned u = a[i], v = a[l];
+          if ((u > v) == ((i & k) == 0)) {
+            a[i] = v;
+            a[l] = u;
+          }
+        }
+      }
+      __syncthreads();
+    }
 }
 
 __global__ void __launch_bounds__(kClusterThreads)
     cluster_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm,
                    int rows_base, int rows, int window, int n_windows, int leaf, double cx,
                    double cy, double inv_extent, int kBI) {
-  // dynamic shared memory (aliases the exp table of other kernels): packed
-  // keys (x << 16 | y) and row indices within the window
-  unsigned* kxy = reinterpret_cast<unsigned*>(s_exp2_tab);
-  unsigned short* kv = reinterpret_cast<unsigned short*>(kxy + window);
+  // dynamic shared memory (aliases the exp table of other kernels):
+  //   kc [window] u32 composite keys; after the sorts its first half holds the
+  //      y-sorted indices and its second half the partition scratch
+  //   lx [window] u16 x-sorted indices, flags [window/32], pre [window/32]
+  unsigned* kc = reinterpret_cast<unsigned*>(s_exp2_tab);
+  unsigned short* lx = reinterpret_cast<unsigned short*>(kc + window);
+  unsigned* flags = reinterpret_cast<unsigned*>(lx + window);
+  int* pre = reinterpret_cast<int*>(flags + window / 32);
+  __shared__ int s_wsum[kClusterThreads / 32];
   // window blockIdx.x: rows [w0, w1) of the shard, sorted into rperm slots
   // [blockIdx.x * window, + window)
-  // windows are whole groups of kBI-row blocks (the varying plan's 256-row
-  // blocks, or the trigger expansion's 2048-row checkpoints)
+  // windows are whole groups of kBI-row blocks (the varying plan's blocks,
+  // or the trigger expansion's checkpoints)
   const int nblocks = (rows + kBI - 1) / kBI;
   const int w0 = window_first_block(blockIdx.x, nblocks, n_windows) * kBI;
   const int w1 = min(rows, window_first_block(blockIdx.x + 1, nblocks, n_windows) * kBI);
   const int window_rows = w1 - w0;
-  HK_ASSERT(window <= kMaxClusterWindow && window % leaf == 0 && window_rows <= window &&
-            blockDim.x == kClusterThreads);
-  for (int i = threadIdx.x; i < window; i += kClusterThreads) {
-    const bool ok = i < window_rows;
-    const int row = rows_base + w0 + i;
-    kxy[i] = ok ? (quantise16(x[row], cx, inv_extent) << 16) | quantise16(y[row], cy, inv_extent)
-                : 0xffffffffu;
-    kv[i] = ok ? static_cast<unsigned short>(i) : 0xffff;
-  }
+  const int tid = threadIdx.x, nw = window / 32;
+  HK_ASSERT(window <= kMaxClusterWindow && window % leaf == 0 && leaf >= 32 && window_rows <= window &&
+            blockDim.x == kClusterThreads && nw <= kClusterThreads);
+  auto load_keys = [&](const double* v, double c) {
+    for (int i = tid; i < window; i += kClusterThreads) {
+      const unsigned q = i < window_rows ? quantise16(v[rows_base + w0 + i], c, inv_extent) : 0xffffu;
+      kc[i] = (q << 16) | static_cast<unsigned>(i);
+    }
+    __syncthreads();
+    bitonic_sort_u32(kc, window);
+  };
+  load_keys(x, cx);
+  for (int i = tid; i < window; i += kClusterThreads) lx[i] = static_cast<unsigned short>(kc[i] & 0xffffu);
   __syncthreads();
-  int level = 0;
-  for (int S = window; S > leaf; S >>= 1, ++level) {
-    const int shift = (level & 1) ? 0 : 16;  // x first, then y, ...
-    for (int k = 2; k <= S; k <<= 1) {
-      for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < window; i += kClusterThreads) {
-          const int l = i ^ j;
-          if (l > i) {
-            const bool up = k == S || (i & k) == 0;
-            const unsigned a = kxy[i], b = kxy[l];
-            if ((((a >> shift) & 0xffffu) > ((b >> shift) & 0xffffu)) == up) {
-              kxy[i] = b;
-              kxy[l] = a;
-              const unsigned short t = kv[i];
-              kv[i] = kv[l];
-              kv[l] = t;
-            }
-          }
-        }
-        __syncthreads();
+  load_keys(y, cy);
+  {  // the y-sorted indices into kc's first half (through registers: the halves overlap)
+    constexpr int kPer = kMaxClusterWindow / kClusterThreads;
+    unsigned short v[kPer];
+#pragma unroll
+    for (int c = 0; c < kPer; ++c) {
+      const int i = tid + c * kClusterThreads;
+      v[c] = i < window ? static_cast<unsigned short>(kc[i] & 0xffffu) : 0;
+    }
+    __syncthreads();
+    unsigned short* ly = reinterpret_cast<unsigned short*>(kc);
+#pragma unroll
+    for (int c = 0; c < kPer; ++c) {
+      const int i = tid + c * kClusterThreads;
+      if (i < window) ly[i] = v[c];
+    }
+    __syncthreads();
+  }
+  unsigned short* sl = lx;                                        // sorted along this level's axis
+  unsigned short* ol = reinterpret_cast<unsigned short*>(kc);     // sorted along the other axis
+  unsigned short* nl = reinterpret_cast<unsigned short*>(kc) + window;  // scratch
+  for (int S = window; S > leaf; S >>= 1) {
+    const int half = S >> 1;
+    // membership: the first half of every segment of the split list
+    for (int w = tid; w < nw; w += kClusterThreads) flags[w] = 0u;
+    __syncthreads();
+    for (int p = tid; p < window; p += kClusterThreads)
+      if ((p & (S - 1)) < half) atomicOr(&flags[sl[p] >> 5], 1u << (sl[p] & 31));  // integer: order-free
+    __syncthreads();
+    // stable partition of the other list within its segments (S >= 64: a
+    // 32-position word never straddles a segment)
+    unsigned m = 0u;
+    if (tid < nw)
+#pragma unroll 8
+      for (int b = 0; b < 32; ++b) {
+        const unsigned e = ol[tid * 32 + b];
+        m |= ((flags[e >> 5] >> (e & 31)) & 1u) << b;
+      }
+    const int cnt = __popc(m);
+    int inc = cnt;  // block-wide inclusive scan of the words' counts
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, off);
+      if ((tid & 31) >= off) inc += t;
+    }
+    if ((tid & 31) == 31) s_wsum[tid >> 5] = inc;
+    __syncthreads();
+    if (tid < 32) {
+      int ws = s_wsum[tid];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, ws, off);
+        if (tid >= off) ws += t;
+      }
+      s_wsum[tid] = ws;  // inclusive over warps
+    }
+    __syncthreads();
+    const int ex = inc - cnt + ((tid >> 5) ? s_wsum[(tid >> 5) - 1] : 0);
+    if (tid < nw) pre[tid] = ex;
+    __syncthreads();
+    if (tid < nw) {
+      const int s0 = (tid * 32) & ~(S - 1);
+      const int lbase = ex - pre[s0 >> 5];  // left entries of the segment before this word
+#pragma unroll 8
+      for (int b = 0; b < 32; ++b) {
+        const int p = tid * 32 + b;
+        const int lr = lbase + __popc(m & ((1u << b) - 1u));
+        const int dst = ((m >> b) & 1u) ? s0 + lr : s0 + half + (p - s0 - lr);
+        nl[dst] = ol[p];
       }
     }
+    __syncthreads();
+    unsigned short* t = sl;  // next level: split the partitioned list along the other axis
+    sl = nl;
+    nl = ol;
+    ol = t;
   }
-  for (int i = threadIdx.x; i < window; i += kClusterThreads)
-    rperm[blockIdx.x * window + i] = kv[i] == 0xffff ? -1 : rows_base + w0 + kv[i];
+  for (int i = tid; i < window; i += kClusterThreads) {
+    const int e = sl[i];
+    rperm[blockIdx.x * window + i] = e >= window_rows ? -1 : rows_base + w0 + e;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1364,7 +1450,7 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
   if (window > kMaxClusterWindow || window < leaf || window % leaf)
     throw std::invalid_argument("launch_cluster: unsupported window of " + std::to_string(window) +
                                 " rows");
-  const int bytes = window * 6;
+  const int bytes = window * 6 + (window / 32) * 8;  // kc, lx, flags, pre (cluster_kernel)
   const double inv_extent = half_extent > 0.0 ? 1.0 / half_extent : 0.0;
   cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   cluster_kernel<<<n_windows, kClusterThreads, bytes, s>>>(x, y, rperm, rows_base, rows, window,

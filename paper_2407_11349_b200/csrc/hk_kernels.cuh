@@ -125,7 +125,7 @@ void launch_prep_cells(const DeviceCatalog& d, const EvalCoef& c, const CellLayo
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, double half_extent,
                     cudaStream_t s, int block_rows = 0);
-constexpr int kMaxClusterWindow = 32768;  // rows (6 bytes each: 192 KB of dynamic shared memory)
+constexpr int kMaxClusterWindow = 32768;  // rows (6.25 bytes each: 200 KB of dynamic shared memory)
 // Windows of at most max_blocks row blocks covering nblocks: their number,
 // the first block of window w, and the window of block b.
 __host__ __device__ inline int window_count(int nblocks, int max_blocks) {
