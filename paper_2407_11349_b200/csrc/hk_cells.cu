@@ -53,16 +53,28 @@ __global__ void cells_count_kernel(const double* __restrict__ x, const double* _
 }
 
 // per cell: exclusive prefix over the chunks (in place), the cell's count,
-// then (one thread) the cells' first cell-tile positions
-__global__ void cells_scan_kernel(int n_chunks, int ncell, int* chunk_counts, int* cell_start, int* n_ctiles) {
-  for (int c = threadIdx.x; c < ncell; c += blockDim.x) {
-    int acc = 0;
-    for (int k = 0; k < n_chunks; ++k) {
-      const int v = chunk_counts[static_cast<size_t>(k) * ncell + c];
-      chunk_counts[static_cast<size_t>(k) * ncell + c] = acc;
-      acc += v;
+// then (one thread) the cells' first cell-tile positions.  One warp per cell
+// (cells strided over the CTA's warps), 32 chunks per step.
+constexpr int kScanThreads = 1024;
+__global__ void __launch_bounds__(kScanThreads) cells_scan_kernel(int n_chunks, int ncell, int* chunk_counts,
+                                                                  int* cell_start, int* n_ctiles) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = warp; c < ncell; c += kScanThreads / 32) {
+    int carry = 0;
+    for (int k0 = 0; k0 < n_chunks; k0 += 32) {
+      const int k = k0 + lane;
+      int* slot = chunk_counts + static_cast<size_t>(k) * ncell + c;
+      const int v = k < n_chunks ? *slot : 0;
+      int inc = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += t;
+      }
+      if (k < n_chunks) *slot = carry + inc - v;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    cell_start[c] = acc;  // the count, for now
+    if (lane == 0) cell_start[c] = carry;  // the count, for now
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -107,7 +119,7 @@ void launch_cells(const double* x, const double* y, int n, const CellGrid& g, in
   const int n_chunks = (n + kRankChunk - 1) / kRankChunk;
   cudaMemsetAsync(perm, 0xff, static_cast<size_t>(perm_len) * sizeof(int), s);  // -1: padding
   cells_count_kernel<<<n_chunks, 256, ncell * sizeof(int), s>>>(x, y, n, g, cell, chunk_counts);
-  cells_scan_kernel<<<1, 256, 0, s>>>(n_chunks, ncell, chunk_counts, cell_start, n_ctiles);
+  cells_scan_kernel<<<1, kScanThreads, 0, s>>>(n_chunks, ncell, chunk_counts, cell_start, n_ctiles);
   cells_rank_kernel<<<n_chunks, 32, ncell * sizeof(int), s>>>(n, ncell, cell, chunk_counts, cell_start, perm);
 }
 
