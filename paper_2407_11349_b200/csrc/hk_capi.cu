@@ -850,7 +850,9 @@ struct hk_ctx {
       if (const char* e = std::getenv("HK_FGT_ROW_TOL")) G.row_tol = std::atof(e);
       G.mom = s.bgf_mom;
       G.count = s.bgf_count;
-      timed_pair(s, 1, [&] { hk::launch_bg_fgt(G, s.rb, rows, s.bg_sums[bgi], s.fgt_flag, s.stream); });
+      timed_pair(s, 1, [&] {
+        hk::launch_bg_fgt(G, s.rb, rows, s.bg_sums[bgi], s.fgt_flag, s.stream, t[s.rb], t[s.re - 1]);
+      });
       prof_total += 2;
       halves &= ~hk::kHalfBg;  // the pair kernels compute the trigger only
     }
@@ -930,7 +932,7 @@ struct hk_ctx {
       double tol = hk::kFgtRowTol;
       if (const char* e = std::getenv("HK_FGT_ROW_TOL")) tol = std::atof(e);
       hk::launch_tr_cut_cert(dc, c, s.bg_sums[bgi], s.tr_sums[tri], s.rb, rows, s.cert_scratch, tol,
-                             s.fgt_flag, s.stream);
+                             s.fgt_flag, s.stream, lb[s.re - 1]);
       prof_total += 3;
     }
     if (use_fgt || use_bgf || use_cut)

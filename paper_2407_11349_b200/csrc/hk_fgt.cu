@@ -533,10 +533,10 @@ constexpr int kBgThreads = 256;
 
 // box ranges (binary search of each box's first time) and moments: one CTA
 // per box; thread-strided partial sums reduced in a fixed tree order
-__global__ void __launch_bounds__(kBgThreads) bg_fgt_moments_kernel(const BgFgtParams F) {
+__global__ void __launch_bounds__(kBgThreads) bg_fgt_moments_kernel(const BgFgtParams F, int b_lo) {
   __shared__ double s_red[kBgThreads];
   __shared__ int s_range[2];
-  const int b = blockIdx.x;
+  const int b = b_lo + blockIdx.x;
   if (threadIdx.x < 2) {
     const int box = b + threadIdx.x;  // first index whose box >= `box`
     int lo = 0, hi = F.n;
@@ -700,8 +700,13 @@ double bg_fgt_truncation_bound(int p, double gamma) {
 }
 
 void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* bg_sums, unsigned* flag,
-                   cudaStream_t s) {
-  bg_fgt_moments_kernel<<<F.nbt, kBgThreads, 0, s>>>(F);
+                   cudaStream_t s, double t_first, double t_last) {
+  // only the boxes the rows can reach (bg_fgt_eval_kernel's [b0, b1] for the
+  // first and last row; a shard's rows span part of the catalog)
+  const double reach = std::sqrt(kFgtCut) / F.inv_sqd + 0.5 * F.L;
+  const int b_lo = std::max(0, static_cast<int>(std::floor((t_first - reach - F.t0) / F.L)));
+  const int b_hi = std::min(F.nbt - 1, static_cast<int>(std::floor((t_last + reach - F.t0) / F.L)));
+  if (b_hi >= b_lo) bg_fgt_moments_kernel<<<b_hi - b_lo + 1, kBgThreads, 0, s>>>(F, b_lo);
   bg_fgt_eval_kernel<<<(rows_total + kBgThreads - 1) / kBgThreads, kBgThreads, 0, s>>>(F, rows_base, rows_total,
                                                                                      bg_sums, flag);
 }

@@ -69,9 +69,11 @@ struct BgFgtParams {
   int* count;                   // [nbt] columns per box
 };
 double bg_fgt_truncation_bound(int p, double gamma);
-// moments + the rows [rows_base, rows_base + rows_total): bg_sums planes B, B2.
+// moments (of the boxes within reach of times [t_first, t_last]: the rows'
+// first and last) + the rows [rows_base, rows_base + rows_total): bg_sums
+// planes B, B2.
 void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* bg_sums, unsigned* flag,
-                   cudaStream_t s);
+                   cudaStream_t s, double t_first, double t_last);
 
 // eps_p of hk_fgt.cu for p terms and box side gamma sqrt(delta).
 double fgt_truncation_bound(int p, double gamma);

@@ -59,10 +59,13 @@ constexpr double kCostBetaFgt = 0.0;
 inline double background_cost(std::size_t n) {
   return n >= kExpansionRows ? kCostAlphaExpanded : kCostAlphaDirect;
 }
-// The density-scaled kernel culls its trigger spatially: per earlier row it
-// costs ~4.3 (least-squares fit of full(e) = a e + b e^2/2 to the LL+grad
-// times of row prefixes [0, e) at N=1e6: a = 15.6 ms, b = 67.6 ms).
-constexpr double kCostBetaVarying = 4.3;
+// The density-scaled kernel culls its trigger spatially (cell tiles, the
+// certified cut), so a row's cost is nearly proportional to its earlier
+// sources: fit of the shard times at N=1e6 (g = 2, 4, 8) to f + b sum(lb):
+// b = 18.1 ms per 1e12, the per-row part indistinguishable from 0; with
+// beta = 20 the fitted model's max/mean is 1.02-1.03 (4.3 before the cells:
+// measured 1.38 at g = 8).
+constexpr double kCostBetaVarying = 20.0;
 std::vector<std::size_t> plan_shards(const std::vector<int>& lb, std::size_t g,
                                      double beta = kCostBeta);
 

@@ -1363,10 +1363,59 @@ __global__ void cert_decay_kernel(const DeviceCatalog d, const EvalCoef c, doubl
   chunk[2 * n_chunks + k] = exp(-c.omega * (tn - d.t[j0]));  // the carry's decay across the chunk
 }
 
-__global__ void cert_scan_kernel(const double* chunk, double* pre, int n_chunks) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double p = 0.0;
-  for (int k = 0; k < n_chunks; ++k) {
+// The affine recurrence p_{k+1} = p_k a_k + b_k (a_k: the carry's decay
+// across chunk k, b_k: chunk k's own decayed sum), p_0 = 0: each thread
+// composes a contiguous run of chunks, a block-wide scan composes the runs
+// (fixed tree: deterministic), then each thread replays its run.
+constexpr int kCertScanThreads = 1024;
+__global__ void __launch_bounds__(kCertScanThreads) cert_scan_kernel(const double* chunk, double* pre, int n_chunks) {
+  __shared__ double s_a[kCertScanThreads / 32], s_b[kCertScanThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n_chunks + kCertScanThreads - 1) / kCertScanThreads;
+  const int k0 = min(n_chunks, tid * per), k1 = min(n_chunks, k0 + per);
+  double A = 1.0, B = 0.0;  // the run as p -> p A + B
+  for (int k = k0; k < k1; ++k) {
+    A *= chunk[2 * n_chunks + k];
+    B = fma(B, chunk[2 * n_chunks + k], chunk[2 * k]);
+  }
+  // inclusive scan within the warp: (A1, B1) then (A2, B2) = (A1 A2, B1 A2 + B2)
+  double iA = A, iB = B;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const double pA = __shfl_up_sync(0xffffffffu, iA, off), pB = __shfl_up_sync(0xffffffffu, iB, off);
+    if (lane >= off) {
+      iB = fma(pB, iA, iB);
+      iA = pA * iA;
+    }
+  }
+  if (lane == 31) {
+    s_a[warp] = iA;
+    s_b[warp] = iB;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double wA = s_a[lane], wB = s_b[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const double pA = __shfl_up_sync(0xffffffffu, wA, off), pB = __shfl_up_sync(0xffffffffu, wB, off);
+      if (lane >= off) {
+        wB = fma(pB, wA, wB);
+        wA = pA * wA;
+      }
+    }
+    s_a[lane] = wA;  // inclusive over warps
+    s_b[lane] = wB;
+  }
+  __syncthreads();
+  // exclusive prefix of this thread's run, from p_0 = 0: only B matters
+  double eA = __shfl_up_sync(0xffffffffu, iA, 1), eB = __shfl_up_sync(0xffffffffu, iB, 1);
+  if (lane == 0) {
+    eA = 1.0;
+    eB = 0.0;
+  }
+  double p = eB;
+  if (warp > 0) p = fma(s_b[warp - 1], eA, eB);
+  for (int k = k0; k < k1; ++k) {
     pre[k] = p;
     p = fma(p, chunk[2 * n_chunks + k], chunk[2 * k]);
   }
@@ -1552,13 +1601,15 @@ void launch_sum6(const double* parts, int n_dev, double* total, cudaStream_t s) 
 
 void launch_tr_cut_cert(const DeviceCatalog& d, const EvalCoef& c, const double* bg_sums,
                         const double* tr_sums, int rows_base, int rows_total, double* scratch,
-                        double row_tol, unsigned* flag, cudaStream_t s) {
-  const int n_chunks = (d.n + kCertChunk - 1) / kCertChunk;
+                        double row_tol, unsigned* flag, cudaStream_t s, int lb_last) {
+  // the chunks up to the shard's last row's (later sources never precede a row)
+  int n_chunks = (d.n + kCertChunk - 1) / kCertChunk;
+  if (lb_last >= 0) n_chunks = min(n_chunks, lb_last / kCertChunk + 1);
   double* chunk = scratch;               // [n_chunks][2], then [n_chunks] decays
   double* pre = scratch + 3 * n_chunks;  // [n_chunks]
   cert_chunk_kernel<<<n_chunks, 256, 0, s>>>(d, c, chunk);
   cert_decay_kernel<<<(n_chunks + 255) / 256, 256, 0, s>>>(d, c, chunk, n_chunks);
-  cert_scan_kernel<<<1, 32, 0, s>>>(chunk, pre, n_chunks);
+  cert_scan_kernel<<<1, kCertScanThreads, 0, s>>>(chunk, pre, n_chunks);
   cert_rows_kernel<<<(rows_total + 255) / 256, 256, 0, s>>>(d, c, bg_sums, tr_sums, rows_base, rows_total, chunk,
                                                            pre, row_tol, flag);
 }

@@ -161,7 +161,9 @@ void launch_reduce(const double* blockpart, int n_blocks, double* out6, cudaStre
 constexpr int kCertChunk = 1024;
 void launch_tr_cut_cert(const DeviceCatalog& d, const EvalCoef& c, const double* bg_sums,
                         const double* tr_sums, int rows_base, int rows_total, double* scratch,
-                        double row_tol, unsigned* flag, cudaStream_t s);
+                        double row_tol, unsigned* flag, cudaStream_t s, int lb_last = -1);
+// (lb_last: count_before of the shard's last row; the later chunks are left
+// out, -1: every chunk)
 // Bounding box and finiteness of n locations: out5 = {xmin, xmax, ymin, ymax,
 // index of the first non-finite location or n}, on the device; scratch holds
 // bbox_scratch_doubles() doubles.
