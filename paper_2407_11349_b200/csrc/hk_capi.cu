@@ -503,7 +503,24 @@ struct hk_ctx {
       // most one partial tile
       int gc = n < 150000 ? 1 : n < 600000 ? 2 : n < 900000 ? 4 : 8;
       if (const char* e = std::getenv("HK_CELL_GC")) gc = std::min(64, std::max(1, std::atoi(e)));  // tuning
-      const int ncell = gc * gc;
+      // reach classes: each cell's sources split into bands of log density
+      // (a source's reach scales as 1/sqrt(q)), so a cell tile's largest
+      // threshold is not set by one low-density source among many local ones
+      // (N=1e6, trigger ms for 1/2/4/8 classes: bench catalog
+      // 8.37/8.21/8.27/8.46, county 52.8/51.5/51.6/52.6; N=1e5 county with 4:
+      // 1.06 -> 1.17): two from gc = 8
+      int ncls = gc >= 8 ? 2 : 1;
+      if (const char* e = std::getenv("HK_CELL_CLASSES")) ncls = std::min(16, std::max(1, std::atoi(e)));  // tuning
+      double qmin = d[0], qmax = d[0];
+      for (double v : d) {
+        qmin = std::min(qmin, v);
+        qmax = std::max(qmax, v);
+      }
+      if (!(qmin > 0.0) || !(qmax > qmin)) ncls = 1;  // one density (or invalid): no classes
+      s.cgrid.ncls = ncls;
+      s.cgrid.lq0 = ncls > 1 ? std::log(qmin) : 0.0;
+      s.cgrid.inv_lq = ncls > 1 ? ncls / (std::log(qmax) - std::log(qmin)) : 0.0;
+      const int ncell = gc * gc * ncls;
       const int max_tiles = (n + hk::kBJ - 1) / hk::kBJ + ncell;
       const std::size_t npos = static_cast<std::size_t>(max_tiles) * hk::kBJ;
       s.cgrid.gc = gc;
@@ -815,7 +832,7 @@ struct hk_ctx {
       s.cgrid.x0 = cx - half_extent;
       s.cgrid.y0 = cy - half_extent;
       s.cgrid.inv_side = side > 0.0 ? 1.0 / side : 0.0;
-      hk::launch_cells(s.x, s.y, n, s.cgrid, s.cell_id, s.cell_chunk, s.cell_start, s.cell_perm,
+      hk::launch_cells(s.x, s.y, s.q, n, s.cgrid, s.cell_id, s.cell_chunk, s.cell_start, s.cell_perm,
                        s.cells.max_tiles * hk::kBJ, s.cell_nct, s.stream);
       s.cells_loc = loc_version;
       prof_total += 3;

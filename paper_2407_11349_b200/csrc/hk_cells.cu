@@ -28,22 +28,23 @@ namespace {
 
 constexpr int kRankChunk = 1024;
 
-__device__ __forceinline__ int cell_of(double x, double y, const CellGrid& g) {
+__device__ __forceinline__ int cell_of(double x, double y, double q, const CellGrid& g) {
   const int cx = min(max(static_cast<int>(floor((x - g.x0) * g.inv_side)), 0), g.gc - 1);
   const int cy = min(max(static_cast<int>(floor((y - g.y0) * g.inv_side)), 0), g.gc - 1);
-  return cx + g.gc * cy;
+  const int cl = g.ncls > 1 ? min(max(static_cast<int>(floor((log(q) - g.lq0) * g.inv_lq)), 0), g.ncls - 1) : 0;
+  return (cx + g.gc * cy) * g.ncls + cl;
 }
 
 // per chunk of kRankChunk columns: the count of each cell
-__global__ void cells_count_kernel(const double* __restrict__ x, const double* __restrict__ y, int n,
-                                   CellGrid g, int* cell, int* chunk_counts) {
+__global__ void cells_count_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                   const double* __restrict__ q, int n, CellGrid g, int* cell, int* chunk_counts) {
   extern __shared__ int s_cnt[];
-  const int ncell = g.gc * g.gc;
+  const int ncell = g.gc * g.gc * g.ncls;
   for (int c = threadIdx.x; c < ncell; c += blockDim.x) s_cnt[c] = 0;
   __syncthreads();
   const int j0 = blockIdx.x * kRankChunk;
   for (int j = j0 + threadIdx.x; j < min(n, j0 + kRankChunk); j += blockDim.x) {
-    const int c = cell_of(x[j], y[j], g);
+    const int c = cell_of(x[j], y[j], q[j], g);
     cell[j] = c;
     atomicAdd(&s_cnt[c], 1);  // integer counts: order-independent
   }
@@ -113,12 +114,12 @@ __global__ void cells_rank_kernel(int n, int ncell, const int* __restrict__ cell
 
 }  // namespace
 
-void launch_cells(const double* x, const double* y, int n, const CellGrid& g, int* cell, int* chunk_counts,
+void launch_cells(const double* x, const double* y, const double* q, int n, const CellGrid& g, int* cell, int* chunk_counts,
                   int* cell_start, int* perm, int perm_len, int* n_ctiles, cudaStream_t s) {
-  const int ncell = g.gc * g.gc;
+  const int ncell = g.gc * g.gc * g.ncls;
   const int n_chunks = (n + kRankChunk - 1) / kRankChunk;
   cudaMemsetAsync(perm, 0xff, static_cast<size_t>(perm_len) * sizeof(int), s);  // -1: padding
-  cells_count_kernel<<<n_chunks, 256, ncell * sizeof(int), s>>>(x, y, n, g, cell, chunk_counts);
+  cells_count_kernel<<<n_chunks, 256, ncell * sizeof(int), s>>>(x, y, q, n, g, cell, chunk_counts);
   cells_scan_kernel<<<1, kScanThreads, 0, s>>>(n_chunks, ncell, chunk_counts, cell_start, n_ctiles);
   cells_rank_kernel<<<n_chunks, 32, ncell * sizeof(int), s>>>(n, ncell, cell, chunk_counts, cell_start, perm);
 }

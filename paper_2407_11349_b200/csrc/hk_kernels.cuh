@@ -86,6 +86,8 @@ struct DeviceCatalog {
 struct CellGrid {
   int gc;                       // cells per side
   double x0, y0, inv_side;      // grid origin, 1 / cell side
+  int ncls;                     // reach classes per cell (log density bands), 1: none
+  double lq0, inv_lq;           // class = floor((log q - lq0) * inv_lq)
 };
 struct CellLayout {
   const int* perm;              // [npos] position -> column (-1: padding)
@@ -100,7 +102,7 @@ struct CellLayout {
   float* r2;
   double *tmin, *tmax;
 };
-void launch_cells(const double* x, const double* y, int n, const CellGrid& g, int* cell, int* chunk_counts,
+void launch_cells(const double* x, const double* y, const double* q, int n, const CellGrid& g, int* cell, int* chunk_counts,
                   int* cell_start, int* perm, int perm_len, int* n_ctiles, cudaStream_t s);
 
 // Row-sum halves: the background [B, B2] and the trigger [T, Td, Tq].
