@@ -308,3 +308,17 @@ def test_fgt_adaptive_truncation_matches_full_square(eng, monkeypatch, n):
     b = full.eval(p, grad=True)
     assert full.fgt_stats()[:2] == (1, 0)
     close(a, b)
+
+
+@pytest.mark.parametrize("kind", ["bench", "county"])
+def test_cells_reach_classes(eng, monkeypatch, kind):
+    """Cells split into log-density reach classes (HK_CELL_CLASSES; the
+    default at N >= 9e5 is two): the same sums as the time-ordered tiles."""
+    monkeypatch.setenv("HK_CELL_GC", "8")
+    monkeypatch.setenv("HK_CELL_CLASSES", "3")
+    cat = eng.benchmark_catalog(120000, 6) if kind == "bench" else county_like(eng, 120000, seed=7)
+    p = eng.HawkesParams(**BENCH, variant=eng.Variant.varying)
+    ev = eng.Evaluator(cat)
+    a = ev.eval(p, grad=True)
+    ev.set_cells(False)
+    close(a, ev.eval(p, grad=True))
