@@ -397,23 +397,81 @@ __global__ void __launch_bounds__(kFgtEvalThreads, kFgtEvalMinBlocks)
     mbar_init(&s_bar[1], 1);
     mbar_fence_init();
   }
+  // the boxes some row of the CTA can use (the per-row test below, on the
+  // CTA's bounding box with a margin): the others are neither staged nor
+  // visited.  A skipped box changes no row's sums.
+  __shared__ int s_boxes[kFgtMaxBoxes];
+  __shared__ int s_nboxes;
+  __shared__ double s_bb[4][kFgtEvalThreads / 32];
+  {
+    const double kInfD = __longlong_as_double(0x7ff0000000000000LL);
+    double x0 = kInfD, x1 = -kInfD, y0 = kInfD, y1 = -kInfD;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (valid[r]) {
+        x0 = fmin(x0, xi[r]);
+        x1 = fmax(x1, xi[r]);
+        y0 = fmin(y0, yi[r]);
+        y1 = fmax(y1, yi[r]);
+      }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      x0 = fmin(x0, __shfl_xor_sync(0xffffffffu, x0, off));
+      x1 = fmax(x1, __shfl_xor_sync(0xffffffffu, x1, off));
+      y0 = fmin(y0, __shfl_xor_sync(0xffffffffu, y0, off));
+      y1 = fmax(y1, __shfl_xor_sync(0xffffffffu, y1, off));
+    }
+    if (lane == 0) {
+      s_bb[0][warp] = x0;
+      s_bb[1][warp] = x1;
+      s_bb[2][warp] = y0;
+      s_bb[3][warp] = y1;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int w = 1; w < kFgtEvalThreads / 32; ++w) {
+        x0 = fmin(x0, s_bb[0][w]);
+        x1 = fmax(x1, s_bb[1][w]);
+        y0 = fmin(y0, s_bb[2][w]);
+        y1 = fmax(y1, s_bb[3][w]);
+      }
+      int base = 0;
+      for (int B0 = 0; B0 < F.nbox; B0 += 32) {
+        const int B = B0 + lane;
+        bool keep = false;
+        if (B < F.nbox) {
+          const double cxB = F.x0 + (B % F.nb + 0.5) * F.L, cyB = F.y0 + (B / F.nb + 0.5) * F.L;
+          const double gx = fmax(fmax(x0 - cxB, cxB - x1) * F.inv_sqd - 0.5 * F.L * F.inv_sqd, 0.0);
+          const double gy = fmax(fmax(y0 - cyB, cyB - y1) * F.inv_sqd - 0.5 * F.L * F.inv_sqd, 0.0);
+          keep = fma(gx, gx, gy * gy) <= kFgtCut * (1.0 + 1e-9) + 1e-9;  // margin: a superset of the rows' tests
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (keep) s_boxes[base + __popc(m & ((1u << lane) - 1u))] = B;
+        base += __popc(m);
+      }
+      if (lane == 0) s_nboxes = base;
+    }
+  }
   __syncthreads();
+  const int nbx = s_nboxes;
   const bool any = F.P[k] > 0;  // checkpoint with no earlier columns: nothing to add
   double T[R], Td[R], Tq[R], Tq2[R], w_used[R];  // w_used: box weights (A_00 = sum W) evaluated
 #pragma unroll
   for (int r = 0; r < R; ++r) T[r] = Td[r] = Tq[r] = Tq2[r] = w_used[r] = 0.0;
   const double hs = 0.5 * F.L * F.inv_sqd;  // half box side, scaled
-  if (any) {
+  if (any && nbx > 0) {
     if (threadIdx.x == 0) {
       mbar_expect_tx(&s_bar[0], kBoxBytes);
-      bulk_g2s(s_m[0], mk, kBoxBytes, &s_bar[0]);
+      bulk_g2s(s_m[0], mk + static_cast<size_t>(s_boxes[0]) * 2 * PP, kBoxBytes, &s_bar[0]);
     }
     unsigned phases = 0u;
-    for (int B = 0; B < F.nbox; ++B) {
-      const int st = B & 1;
-      if (B + 1 < F.nbox && threadIdx.x == 0) {
+    for (int ib = 0; ib < nbx; ++ib) {
+      const int B = s_boxes[ib];
+      const int st = ib & 1;
+      if (ib + 1 < nbx && threadIdx.x == 0) {
         mbar_expect_tx(&s_bar[st ^ 1], kBoxBytes);
-        bulk_g2s(s_m[st ^ 1], mk + static_cast<size_t>(B + 1) * 2 * PP, kBoxBytes, &s_bar[st ^ 1]);
+        bulk_g2s(s_m[st ^ 1], mk + static_cast<size_t>(s_boxes[ib + 1]) * 2 * PP, kBoxBytes, &s_bar[st ^ 1]);
       }
       mbar_wait(&s_bar[st], (phases >> st) & 1u);
       phases ^= 1u << st;
