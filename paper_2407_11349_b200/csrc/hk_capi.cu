@@ -194,6 +194,7 @@ struct DeviceState {
   std::size_t fgt_mom_bytes = 0;
   double* bgf_mom = nullptr;  // [nbt][kFgtP]: the background's 1-D expansion
   int* bgf_count = nullptr;   // [nbt]
+  double* bgf_part = nullptr; // [nbt][parts][kFgtP] moment parts
   int bgf_cap = 0;            // boxes allocated
   unsigned* fgt_flag = nullptr;                          // device
   unsigned* h_fgt_flag = nullptr;                        // pinned
@@ -306,7 +307,7 @@ struct hk_ctx {
       for (void* q : {static_cast<void*>(s.ck_P), static_cast<void*>(s.fgt_tR), static_cast<void*>(s.fgt_decay),
                       static_cast<void*>(s.fgt_dt), static_cast<void*>(s.fgt_box), static_cast<void*>(s.fgt_u),
                       static_cast<void*>(s.fgt_v), static_cast<void*>(s.fgt_mom), static_cast<void*>(s.fgt_flag),
-                      static_cast<void*>(s.bgf_mom), static_cast<void*>(s.bgf_count), static_cast<void*>(s.fgt_wsum),
+                      static_cast<void*>(s.bgf_mom), static_cast<void*>(s.bgf_count), static_cast<void*>(s.bgf_part), static_cast<void*>(s.fgt_wsum),
                       static_cast<void*>(s.fgt_perm), static_cast<void*>(s.cert_scratch)})
         if (q) cudaFree(q);
       if (s.h_fgt_flag) cudaFreeHost(s.h_fgt_flag);
@@ -845,11 +846,15 @@ struct hk_ctx {
       if (fgt->nbt > s.bgf_cap) {
         if (s.bgf_mom) ck(cudaFree(s.bgf_mom), "cudaFree");
         if (s.bgf_count) ck(cudaFree(s.bgf_count), "cudaFree");
+        if (s.bgf_part) ck(cudaFree(s.bgf_part), "cudaFree");
         s.bgf_mom = nullptr;
         s.bgf_count = nullptr;
+        s.bgf_part = nullptr;
         s.bgf_cap = 0;
         s.bgf_mom = dmalloc<double>(static_cast<std::size_t>(fgt->nbt) * hk::kFgtP);
         s.bgf_count = dmalloc<int>(fgt->nbt);
+        // parts for any box range: boxes x parts <= max(nbt, n / 4096) (bg_fgt_parts)
+        s.bgf_part = dmalloc<double>(static_cast<std::size_t>(std::max(fgt->nbt, n / 4096 + 1)) * hk::kFgtP);
         s.bgf_cap = fgt->nbt;
       }
       hk::BgFgtParams G{};
@@ -868,7 +873,7 @@ struct hk_ctx {
       G.mom = s.bgf_mom;
       G.count = s.bgf_count;
       timed_pair(s, 1, [&] {
-        hk::launch_bg_fgt(G, s.rb, rows, s.bg_sums[bgi], s.fgt_flag, s.stream, t[s.rb], t[s.re - 1]);
+        hk::launch_bg_fgt(G, s.rb, rows, s.bg_sums[bgi], s.fgt_flag, s.stream, t[s.rb], t[s.re - 1], s.bgf_part);
       });
       prof_total += 2;
       halves &= ~hk::kHalfBg;  // the pair kernels compute the trigger only

@@ -589,12 +589,15 @@ __global__ void fgt_wsum_kernel(const FgtParams F) {
 
 constexpr int kBgThreads = 256;
 
-// box ranges (binary search of each box's first time) and moments: one CTA
-// per box; thread-strided partial sums reduced in a fixed tree order
-__global__ void __launch_bounds__(kBgThreads) bg_fgt_moments_kernel(const BgFgtParams F, int b_lo) {
-  __shared__ double s_red[kBgThreads];
+// box ranges (binary search of each box's first time) and moments: CTA
+// (b, s) sums the s-th of gridDim.y equal parts of box b's columns into
+// part[(b - b_lo) gridDim.y + s] (thread-strided partial sums, warp
+// butterflies, warps in order); bg_fgt_reduce_kernel adds the parts in order.
+// Deterministic for a fixed part count.
+__global__ void __launch_bounds__(kBgThreads) bg_fgt_moments_kernel(const BgFgtParams F, int b_lo, double* part) {
+  __shared__ double s_w[kBgThreads / 32][P];
   __shared__ int s_range[2];
-  const int b = b_lo + blockIdx.x;
+  const int b = b_lo + blockIdx.x, S = gridDim.y, sidx = blockIdx.y;
   if (threadIdx.x < 2) {
     const int box = b + threadIdx.x;  // first index whose box >= `box`
     int lo = 0, hi = F.n;
@@ -607,7 +610,9 @@ __global__ void __launch_bounds__(kBgThreads) bg_fgt_moments_kernel(const BgFgtP
     s_range[threadIdx.x] = box >= F.nbt ? F.n : lo;
   }
   __syncthreads();
-  const int j0 = s_range[0], j1 = s_range[1];
+  const int b0 = s_range[0], b1 = s_range[1];
+  const long long len = b1 - b0;
+  const int j0 = b0 + static_cast<int>(len * sidx / S), j1 = b0 + static_cast<int>(len * (sidx + 1) / S);
   const double c = F.t0 + (b + 0.5) * F.L;
   double acc[P];
 #pragma unroll
@@ -621,18 +626,29 @@ __global__ void __launch_bounds__(kBgThreads) bg_fgt_moments_kernel(const BgFgtP
       pw = pw * u * c_recip.v[n];
     }
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int n = 0; n < P; ++n) {
-    s_red[threadIdx.x] = acc[n];
-    __syncthreads();
-    for (int h = kBgThreads / 2; h > 0; h >>= 1) {
-      if (threadIdx.x < h) s_red[threadIdx.x] += s_red[threadIdx.x + h];
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) F.mom[b * P + n] = s_red[0];
-    __syncthreads();
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc[n] += __shfl_xor_sync(0xffffffffu, acc[n], off);
+    if (lane == 0) s_w[warp][n] = acc[n];
   }
-  if (threadIdx.x == 0) F.count[b] = j1 - j0;
+  __syncthreads();
+  if (threadIdx.x < P) {
+    double v = s_w[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < kBgThreads / 32; ++w) v += s_w[w][threadIdx.x];
+    part[(static_cast<size_t>(blockIdx.x) * S + sidx) * P + threadIdx.x] = v;
+  }
+  if (threadIdx.x == 0 && sidx == 0) F.count[b] = b1 - b0;
+}
+
+__global__ void bg_fgt_reduce_kernel(const BgFgtParams F, int b_lo, int S, const double* __restrict__ part) {
+  const int n = threadIdx.x, bi = blockIdx.x;
+  if (n >= P) return;
+  double v = 0.0;
+  for (int s = 0; s < S; ++s) v += part[(static_cast<size_t>(bi) * S + s) * P + n];
+  F.mom[(b_lo + bi) * P + n] = v;
 }
 
 __global__ void __launch_bounds__(kBgThreads) bg_fgt_eval_kernel(const BgFgtParams F, int rows_base,
@@ -757,14 +773,24 @@ double bg_fgt_truncation_bound(int p, double gamma) {
   return K * tail / (1.0 - rho / std::sqrt(p + 1.0));
 }
 
+int bg_fgt_parts(int n, int boxes) {
+  // about 4096 columns per part, at most 64 parts per box
+  return std::max(1, std::min(64, n / (4096 * std::max(1, boxes))));
+}
+
 void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* bg_sums, unsigned* flag,
-                   cudaStream_t s, double t_first, double t_last) {
+                   cudaStream_t s, double t_first, double t_last, double* part) {
   // only the boxes the rows can reach (bg_fgt_eval_kernel's [b0, b1] for the
   // first and last row; a shard's rows span part of the catalog)
   const double reach = std::sqrt(kFgtCut) / F.inv_sqd + 0.5 * F.L;
   const int b_lo = std::max(0, static_cast<int>(std::floor((t_first - reach - F.t0) / F.L)));
   const int b_hi = std::min(F.nbt - 1, static_cast<int>(std::floor((t_last + reach - F.t0) / F.L)));
-  if (b_hi >= b_lo) bg_fgt_moments_kernel<<<b_hi - b_lo + 1, kBgThreads, 0, s>>>(F, b_lo);
+  if (b_hi >= b_lo) {
+    const int nb = b_hi - b_lo + 1;
+    const int S = bg_fgt_parts(F.n, nb);
+    bg_fgt_moments_kernel<<<dim3(nb, S), kBgThreads, 0, s>>>(F, b_lo, part);
+    bg_fgt_reduce_kernel<<<nb, 32, 0, s>>>(F, b_lo, S, part);
+  }
   bg_fgt_eval_kernel<<<(rows_total + kBgThreads - 1) / kBgThreads, kBgThreads, 0, s>>>(F, rows_base, rows_total,
                                                                                      bg_sums, flag);
 }

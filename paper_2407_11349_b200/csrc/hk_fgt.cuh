@@ -72,8 +72,11 @@ double bg_fgt_truncation_bound(int p, double gamma);
 // moments (of the boxes within reach of times [t_first, t_last]: the rows'
 // first and last) + the rows [rows_base, rows_base + rows_total): bg_sums
 // planes B, B2.
+// part: scratch of boxes x bg_fgt_parts(n, boxes) x kFgtP doubles (boxes: at
+// most nbt).
 void launch_bg_fgt(const BgFgtParams& F, int rows_base, int rows_total, double* bg_sums, unsigned* flag,
-                   cudaStream_t s, double t_first, double t_last);
+                   cudaStream_t s, double t_first, double t_last, double* part);
+int bg_fgt_parts(int n, int boxes);
 
 // eps_p of hk_fgt.cu for p terms and box side gamma sqrt(delta).
 double fgt_truncation_bound(int p, double gamma);
