@@ -123,18 +123,13 @@ constexpr int kMomSmem = kMomWarps * kMomBatch * (3 * P) * static_cast<int>(size
                          kMomSort * static_cast<int>(sizeof(unsigned)) +
                          (kFgtMaxBoxes + 1) * static_cast<int>(sizeof(int));
 
-// adds the batch's sources (in batch order) to the box's coefficients: lane
-// b (< P) owns the coefficients (a, b) of both sets for every a, so per
-// source it reads its v^b/b! once and the broadcast u^a/a! weights
-__device__ __forceinline__ void fgt_flush(double* ob, bool grad, int nb, const double* wpu, const double* pv,
-                                          int lane) {
+// adds the batch's sources (in batch order) to the box's coefficients held
+// in registers: lane b (< P) owns the coefficients (a, b) of both sets for
+// every a, so per source it reads its v^b/b! once and the broadcast u^a/a!
+// weights
+__device__ __forceinline__ void fgt_accumulate(double (&accA)[P], double (&accB)[P], bool grad, int nb,
+                                               const double* wpu, const double* pv, int lane) {
   if (lane >= P) return;
-  double accA[P], accB[P];
-#pragma unroll
-  for (int a = 0; a < P; ++a) {
-    accA[a] = ob[a * P + lane];
-    accB[a] = grad ? ob[PP + a * P + lane] : 0.0;
-  }
   for (int s = 0; s < nb; ++s) {
     const double vb = pv[s * P + lane];
     const double* wa = wpu + s * 2 * P;  // [W u^a / a!, (t_R - t) W u^a / a!]
@@ -143,11 +138,6 @@ __device__ __forceinline__ void fgt_flush(double* ob, bool grad, int nb, const d
       accA[a] = fma(wa[a], vb, accA[a]);
       if (grad) accB[a] = fma(wa[P + a], vb, accB[a]);
     }
-  }
-#pragma unroll
-  for (int a = 0; a < P; ++a) {
-    ob[a * P + lane] = accA[a];
-    if (grad) ob[PP + a * P + lane] = accB[a];
   }
 }
 
@@ -166,11 +156,12 @@ __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParam
   const double tR = F.tR[k];
   const bool grad = F.grad != 0;
   double* out = F.mom + static_cast<size_t>(k) * F.nbox * 2 * PP;
-  for (int c = threadIdx.x; c < F.nbox * 2 * PP; c += kMomThreads)
-    if (grad || c % (2 * PP) < PP) out[c] = 0.0;
+  if (j1 <= j0)  // an empty interval: zero increments
+    for (int c = threadIdx.x; c < F.nbox * 2 * PP; c += kMomThreads)
+      if (grad || c % (2 * PP) < PP) out[c] = 0.0;
   for (int p0 = j0; p0 < j1; p0 += kMomSort) {
     const int cnt = min(kMomSort, j1 - p0);
-    __syncthreads();  // the previous pass is done with keys / start; the zero fill is visible
+    __syncthreads();  // the previous pass is done with keys / start and its stores are visible
     for (int i = threadIdx.x; i < kMomSort; i += kMomThreads)
       keys[i] = i < cnt ? (static_cast<unsigned>(F.box[p0 + i]) << 12) | static_cast<unsigned>(i) : 0xffffffffu;
     HK_ASSERT(j1 <= F.ncols && kMomSort <= 4096);
@@ -202,6 +193,15 @@ __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParam
     __syncthreads();
     for (int B = warp; B < F.nbox; B += kMomWarps) {
       double* ob = out + static_cast<size_t>(B) * 2 * PP;
+      // the box's coefficients stay in registers over its sources: written
+      // once per pass (the first pass starts from zero: no fill, no reload)
+      double accA[P], accB[P];
+      const bool first = p0 == j0;
+#pragma unroll
+      for (int a = 0; a < P; ++a) {
+        accA[a] = (first || lane >= P) ? 0.0 : ob[a * P + lane];
+        accB[a] = (first || lane >= P || !grad) ? 0.0 : ob[PP + a * P + lane];
+      }
       for (int s0 = start[B]; s0 < start[B + 1]; s0 += kMomBatch) {
         const int nb = min(kMomBatch, start[B + 1] - s0);
         if (lane < nb) {
@@ -222,9 +222,15 @@ __global__ void __launch_bounds__(kMomThreads) fgt_moments_kernel(const FgtParam
           }
         }
         __syncwarp();
-        fgt_flush(ob, grad, nb, wpu, pv, lane);
+        fgt_accumulate(accA, accB, grad, nb, wpu, pv, lane);
         __syncwarp();
       }
+      if (lane < P)
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+          ob[a * P + lane] = accA[a];
+          if (grad) ob[PP + a * P + lane] = accB[a];
+        }
     }
   }
 }
