@@ -230,6 +230,10 @@ int hk_eval_rows(hk_ctx* ctx, const hk_params* p, size_t b, size_t e, double* el
  *     so whole tiles beyond a block's reach are skipped; 0 visits them in
  *     time order.  Same sums, different summation order. */
 #define HK_OPT_CELLS 5
+/*   HK_OPT_SINGLE_FP64: Precision::single evaluations of catalogs of at least
+ *     131072 events run the FP64 expansion / cut path (faster there than the
+ *     FP32 direct kernels, and more accurate); 0 keeps the FP32 kernels. */
+#define HK_OPT_SINGLE_FP64 6
 int hk_set_option(hk_ctx* ctx, int option, int value);
 /* Evaluations that used a Hermite expansion (trigger or background),
  * synchronous ones recomputed

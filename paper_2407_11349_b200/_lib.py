@@ -30,6 +30,7 @@ HK_OPT_FGT = 2
 HK_OPT_BG_FGT = 3
 HK_OPT_TR_CUT = 4
 HK_OPT_CELLS = 5
+HK_OPT_SINGLE_FP64 = 6
 
 
 class hk_params(C.Structure):

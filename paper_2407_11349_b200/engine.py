@@ -235,7 +235,8 @@ class Evaluator:
         return (ll.value, g, ell, gr) if grad else (ll.value, ell)
 
     def eval_single(self, params: HawkesParams) -> float:
-        """Precision.single: FP32 trigger arithmetic, log-likelihood only."""
+        """Precision.single, log-likelihood only: FP32 trigger arithmetic, or
+        from 131072 events the FP64 expansion path (HK_OPT_SINGLE_FP64)."""
         p = params.to_c()
         ll = C.c_double()
         check(lib.hk_eval_single(self._h, C.byref(p), C.byref(ll)))
@@ -304,6 +305,10 @@ class Evaluator:
     def set_cells(self, on: bool) -> None:
         """HK_OPT_CELLS: the density-scaled trigger over spatial cell tiles (default on)."""
         check(lib.hk_set_option(self._h, _lib.HK_OPT_CELLS, int(on)))
+
+    def set_single_fp64(self, on: bool) -> None:
+        """HK_OPT_SINGLE_FP64: large Precision.single evaluations through the FP64 expansions (default on)."""
+        check(lib.hk_set_option(self._h, _lib.HK_OPT_SINGLE_FP64, int(on)))
 
     def fgt_stats(self):
         """(evaluations through the expansion, direct recomputations, last

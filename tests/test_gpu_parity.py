@@ -500,14 +500,20 @@ def test_single_precision_acceptance1(eng, case):
 
 @pytest.mark.parametrize("variant", [0, 1])
 def test_single_precision_large(eng, variant):
-    """N=2e5 benchmark catalog: single vs double precision engine, 1e-5."""
+    """N=2e5 benchmark catalog: single vs double precision engine, 1e-5.
+    From 131072 events Precision.single runs the FP64 expansion path
+    (HK_OPT_SINGLE_FP64, default on): bitwise the double LL; with the option
+    off the FP32 kernels, within 1e-5."""
     cat = eng.benchmark_catalog(200000, 9)
     ev = eng.Evaluator(cat)
     p = hp(eng, BENCH, variant)
     d = ev.eval(p)
     f = ev.eval_single(p)
-    assert abs(f - d) <= 1e-5 * abs(d)
-    assert ev.eval_single(p) == f  # deterministic
+    assert f == d
+    ev.set_single_fp64(False)
+    f32 = ev.eval_single(p)
+    assert abs(f32 - d) <= 1e-5 * abs(d) and f32 != d
+    assert ev.eval_single(p) == f32  # deterministic
 
 
 def test_single_precision_adversarial_finite(eng):
