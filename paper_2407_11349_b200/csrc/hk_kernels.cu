@@ -1009,79 +1009,129 @@ __device__ __forceinline__ unsigned quantise16(double v, double c, double inv_ex
   return static_cast<unsigned>(fmin(fmax(q, 0.0), 65534.0));
 }
 
+// Bitonic sort of a[0, n) (n a power of two, n <= E blockDim): thread t owns
+// a[t E, t E + E) in registers, so the stages with j < E (pairs inside one
+// thread's run) are register compare-exchanges with no barrier; only the
+// stages with j >= E go through shared memory.  The same network as the
+// plain smem sort, so the same result.
+template <int E>
 __device__ __forceinline__ void bitonic_sort_u32(unsigned* a, int n) {
-  for (int k = 2; k <= n; k <<= 1)
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned u = a[i], v = a[l];
-          if ((u > v) == ((i & k) == 0)) {
-            a[i] = v;
-            a[l] = u;
+  const int base = threadIdx.x * E;
+  const bool own = base < n;
+  unsigned v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = own ? a[base + e] : 0u;
+  for (int k = 2; k <= n; k <<= 1) {
+    if (k > E) {  // the strides j >= E through shared memory
+      if (own)
+#pragma unroll
+        for (int e = 0; e < E; ++e) a[base + e] = v[e];
+      __syncthreads();
+      for (int j = k >> 1; j >= E; j >>= 1) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          const int l = i ^ j;
+          if (l > i) {
+            const unsigned u = a[i], w = a[l];
+            if ((u > w) == ((i & k) == 0)) {
+              a[i] = w;
+              a[l] = u;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
+      if (own)
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = a[base + e];
     }
+#pragma unroll
+    for (int j = E >> 1; j > 0; j >>= 1) {  // in registers (j < k always: k >= 2j here)
+      if (j >= k) continue;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if (e & j) continue;
+        const bool up = ((base + e) & k) == 0;
+        const unsigned u = v[e], w = v[e ^ j];
+        if ((u > w) == up) {
+          v[e] = w;
+          v[e ^ j] = u;
+        }
+      }
+    }
+  }
+  __syncthreads();  // every thread has read the last smem stage before the stores
+  if (own)
+#pragma unroll
+    for (int e = 0; e < E; ++e) a[base + e] = v[e];
+  __syncthreads();
+}
+
+__device__ __forceinline__ void bitonic_sort_u32_any(unsigned* a, int n) {
+  const int e = n / static_cast<int>(blockDim.x);
+  if (e >= 32) bitonic_sort_u32<32>(a, n);
+  else if (e >= 16) bitonic_sort_u32<16>(a, n);
+  else if (e >= 8) bitonic_sort_u32<8>(a, n);
+  else if (e >= 4) bitonic_sort_u32<4>(a, n);
+  else if (e >= 2) bitonic_sort_u32<2>(a, n);
+  else bitonic_sort_u32<1>(a, n);
+}
+
+// the window's rows [w0, w1) for window blockIdx.x (whole groups of kBI-row
+// blocks: the varying plan's blocks, or the trigger expansion's checkpoints)
+__device__ __forceinline__ void cluster_window(int rows, int n_windows, int kBI, int& w0, int& w1) {
+  const int nblocks = (rows + kBI - 1) / kBI;
+  w0 = window_first_block(blockIdx.x, nblocks, n_windows) * kBI;
+  w1 = min(rows, window_first_block(blockIdx.x + 1, nblocks, n_windows) * kBI);
+}
+
+// One CTA per (window, axis): the window sorted along x (blockIdx.y = 0) or y
+// as 16-bit in-window indices, written into the window's own rperm slots
+// (window ints hold both lists) for cluster_kernel.
+__global__ void __launch_bounds__(kClusterThreads)
+    cluster_sort_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm, int rows_base,
+                        int rows, int window, int n_windows, double cx, double cy, double inv_extent, int kBI) {
+  unsigned* kc = reinterpret_cast<unsigned*>(s_exp2_tab);  // dynamic shared memory: [window] keys
+  int w0, w1;
+  cluster_window(rows, n_windows, kBI, w0, w1);
+  const int window_rows = w1 - w0;
+  HK_ASSERT(window <= kMaxClusterWindow && window_rows <= window && blockDim.x == kClusterThreads);
+  const double* v = blockIdx.y ? y : x;
+  const double c = blockIdx.y ? cy : cx;
+  for (int i = threadIdx.x; i < window; i += kClusterThreads) {
+    const unsigned q = i < window_rows ? quantise16(v[rows_base + w0 + i], c, inv_extent) : 0xffffu;
+    kc[i] = (q << 16) | static_cast<unsigned>(i);
+  }
+  __syncthreads();
+  bitonic_sort_u32_any(kc, window);
+  unsigned short* out = reinterpret_cast<unsigned short*>(rperm + static_cast<size_t>(blockIdx.x) * window) +
+                        static_cast<size_t>(blockIdx.y) * window;
+  for (int i = threadIdx.x; i < window; i += kClusterThreads) out[i] = static_cast<unsigned short>(kc[i] & 0xffffu);
 }
 
 __global__ void __launch_bounds__(kClusterThreads)
-    cluster_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm,
-                   int rows_base, int rows, int window, int n_windows, int leaf, double cx,
-                   double cy, double inv_extent, int kBI) {
-  // dynamic shared memory (aliases the exp table of other kernels):
-  //   kc [window] u32 composite keys; after the sorts its first half holds the
-  //      y-sorted indices and its second half the partition scratch
-  //   lx [window] u16 x-sorted indices, flags [window/32], pre [window/32]
-  unsigned* kc = reinterpret_cast<unsigned*>(s_exp2_tab);
-  unsigned short* lx = reinterpret_cast<unsigned short*>(kc + window);
-  unsigned* flags = reinterpret_cast<unsigned*>(lx + window);
+    cluster_kernel(int* rperm, int rows_base, int rows, int window, int n_windows, int leaf, int kBI) {
+  // dynamic shared memory (aliases the exp table of other kernels): the
+  // x-sorted, y-sorted and scratch index lists, flags [window/32], pre [window/32]
+  unsigned short* lx = reinterpret_cast<unsigned short*>(s_exp2_tab);
+  unsigned short* ly = lx + window;
+  unsigned short* lt = ly + window;
+  unsigned* flags = reinterpret_cast<unsigned*>(lt + window);
   int* pre = reinterpret_cast<int*>(flags + window / 32);
   __shared__ int s_wsum[kClusterThreads / 32];
-  // window blockIdx.x: rows [w0, w1) of the shard, sorted into rperm slots
-  // [blockIdx.x * window, + window)
-  // windows are whole groups of kBI-row blocks (the varying plan's blocks,
-  // or the trigger expansion's checkpoints)
-  const int nblocks = (rows + kBI - 1) / kBI;
-  const int w0 = window_first_block(blockIdx.x, nblocks, n_windows) * kBI;
-  const int w1 = min(rows, window_first_block(blockIdx.x + 1, nblocks, n_windows) * kBI);
+  int w0, w1;
+  cluster_window(rows, n_windows, kBI, w0, w1);
   const int window_rows = w1 - w0;
   const int tid = threadIdx.x, nw = window / 32;
   HK_ASSERT(window <= kMaxClusterWindow && window % leaf == 0 && leaf >= 32 && window_rows <= window &&
             blockDim.x == kClusterThreads && nw <= kClusterThreads);
-  auto load_keys = [&](const double* v, double c) {
-    for (int i = tid; i < window; i += kClusterThreads) {
-      const unsigned q = i < window_rows ? quantise16(v[rows_base + w0 + i], c, inv_extent) : 0xffffu;
-      kc[i] = (q << 16) | static_cast<unsigned>(i);
-    }
-    __syncthreads();
-    bitonic_sort_u32(kc, window);
-  };
-  load_keys(x, cx);
-  for (int i = tid; i < window; i += kClusterThreads) lx[i] = static_cast<unsigned short>(kc[i] & 0xffffu);
-  __syncthreads();
-  load_keys(y, cy);
-  {  // the y-sorted indices into kc's first half (through registers: the halves overlap)
-    constexpr int kPer = kMaxClusterWindow / kClusterThreads;
-    unsigned short v[kPer];
-#pragma unroll
-    for (int c = 0; c < kPer; ++c) {
-      const int i = tid + c * kClusterThreads;
-      v[c] = i < window ? static_cast<unsigned short>(kc[i] & 0xffffu) : 0;
-    }
-    __syncthreads();
-    unsigned short* ly = reinterpret_cast<unsigned short*>(kc);
-#pragma unroll
-    for (int c = 0; c < kPer; ++c) {
-      const int i = tid + c * kClusterThreads;
-      if (i < window) ly[i] = v[c];
-    }
-    __syncthreads();
+  {
+    const unsigned short* in = reinterpret_cast<const unsigned short*>(rperm + static_cast<size_t>(blockIdx.x) * window);
+    for (int i = tid; i < 2 * window; i += kClusterThreads) lx[i] = in[i];  // lx then ly
   }
-  unsigned short* sl = lx;                                        // sorted along this level's axis
-  unsigned short* ol = reinterpret_cast<unsigned short*>(kc);     // sorted along the other axis
-  unsigned short* nl = reinterpret_cast<unsigned short*>(kc) + window;  // scratch
+  __syncthreads();
+  unsigned short* sl = lx;  // sorted along this level's axis
+  unsigned short* ol = ly;  // sorted along the other axis
+  unsigned short* nl = lt;  // scratch
   for (int S = window; S > leaf; S >>= 1) {
     const int half = S >> 1;
     // membership: the first half of every segment of the split list
@@ -1499,12 +1549,16 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
   if (window > kMaxClusterWindow || window < leaf || window % leaf)
     throw std::invalid_argument("launch_cluster: unsupported window of " + std::to_string(window) +
                                 " rows");
-  const int bytes = window * 6 + (window / 32) * 8;  // kc, lx, flags, pre (cluster_kernel)
   const double inv_extent = half_extent > 0.0 ? 1.0 / half_extent : 0.0;
+  const int kbi = block_rows > 0 ? block_rows : rows_per_item(true);
+  // the two sorts of every window in parallel CTAs, then the partitions
+  const int sort_bytes = window * 4;
+  cudaFuncSetAttribute(cluster_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_bytes);
+  cluster_sort_kernel<<<dim3(n_windows, 2), kClusterThreads, sort_bytes, s>>>(x, y, rperm, rows_base, rows, window,
+                                                                               n_windows, cx, cy, inv_extent, kbi);
+  const int bytes = window * 6 + (window / 32) * 8;  // lx, ly, scratch, flags, pre (cluster_kernel)
   cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cluster_kernel<<<n_windows, kClusterThreads, bytes, s>>>(x, y, rperm, rows_base, rows, window,
-                                                           n_windows, leaf, cx, cy, inv_extent,
-                                                           block_rows > 0 ? block_rows : rows_per_item(true));
+  cluster_kernel<<<n_windows, kClusterThreads, bytes, s>>>(rperm, rows_base, rows, window, n_windows, leaf, kbi);
 }
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,
