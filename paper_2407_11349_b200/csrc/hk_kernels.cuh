@@ -27,8 +27,10 @@ constexpr int kMaxItemTiles = 2048;  // te - tb (the pair kernel classifies them
 constexpr int kItemTarget = 148 * 3 * 72;
 // The density-scaled (clustered, trigger-only) plan: half as many items are
 // as fast there (N=1e6: 16000 items 17.48 ms = 31968 items; county catalog
-// +0.5%) and halve its partial-sum traffic.
-constexpr int kItemTargetVarying = 16000;
+// +0.5%) and halve its partial-sum traffic.  Over cell tiles (trigger ms,
+// bench / county catalog): 6000 items 8.07 / 53.1, 12000 8.14 / 51.5,
+// 16000 8.22 / 51.5.
+constexpr int kItemTargetVarying = 12000;
 // Column chunks per row block at most: the partial-sum buffer holds
 // slots x 40 B per row.
 constexpr int kMaxSlots = 64;
