@@ -115,21 +115,23 @@ int guarded(Fn&& fn) {
 }
 
 // Row blocks per clustering window of the varying plan: the largest power
-// of two <= min(64, catalog blocks / 24) (measured: 64 at N=1e6, 16 at
-// N=1e5);
+// of two whose window holds at most kMaxClusterWindow rows and leaves at
+// least ~12 windows (N=1e6: 128 blocks of 256 rows; N=1e5: 32).  With the
+// cell layout the trigger wants the largest windows the clustering can hold
+// (more rows per window: spatially smaller k-d leaves of 64 rows): bench /
+// county catalog trigger ms at N=1e6, 2 rows/thread, 64 blocks 7.95 / 51.2,
+// 128 blocks 5.66 / 45.0; N=1e5 16 blocks 0.40, 32 blocks 0.36.
 // HK_ROW_WINDOW overrides (1 disables the clustering).
 int row_window(int rows) {
   if (const char* e = std::getenv("HK_ROW_WINDOW")) {
     const int w = std::atoi(e);
-    if ((w == 1 || w == 2 || w == 4 || w == 8 || w == 16 || w == 32 || w == 64 || w == 128) &&
-        w * hk::rows_per_item(true) <= hk::kMaxClusterWindow)
+    if (w >= 1 && w <= 1024 && (w & (w - 1)) == 0 && w * hk::rows_per_item(true) <= hk::kMaxClusterWindow)
       return w;
   }
   const int blocks = (rows + hk::rows_per_item(true) - 1) / hk::rows_per_item(true);
-  // 128 measured no better than 64 at N=1e6 (bench -0.7%, county catalog +2%)
-  const int w_max = std::min(64, hk::kMaxClusterWindow / hk::rows_per_item(true));
+  const int w_max = hk::kMaxClusterWindow / hk::rows_per_item(true);
   int w = 1;
-  while (w < w_max && 2 * w * 24 <= blocks) w *= 2;
+  while (w < w_max && 2 * w * 12 <= blocks) w *= 2;
   return w;
 }
 

@@ -59,7 +59,7 @@ namespace hk {
 #define HK_ROWS_CONST 4
 #endif
 #ifndef HK_ROWS_VAR
-#define HK_ROWS_VAR 4
+#define HK_ROWS_VAR 2
 #endif
 #ifndef HK_UNROLL
 #define HK_UNROLL 4
@@ -74,7 +74,7 @@ __host__ __device__ constexpr int rows_per_item(bool varying) {
 }
 // resident CTAs per SM the register budget is sized for (64K regs)
 #ifndef HK_MIN_BLOCKS_TRIG
-#define HK_MIN_BLOCKS_TRIG 4  // density-scaled trigger-only launches
+#define HK_MIN_BLOCKS_TRIG 5  // density-scaled trigger-only launches
 #endif
 #ifndef HK_MIN_BLOCKS_CONST
 #define HK_MIN_BLOCKS_CONST 3
