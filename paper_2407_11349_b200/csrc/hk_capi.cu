@@ -498,21 +498,22 @@ struct hk_ctx {
     }
     if (s.window > 1) {
       // spatial cell tiles of the density-scaled FP64 trigger: a gc x gc grid
-      // by catalog size (measured on the bench catalog, trigger ms: N=1e5
-      // gc 1/2/4 = 0.53/0.55/0.76, county 1.05/1.19/1.37; 3e5 gc 1/2/4 =
-      // 2.32/2.13/2.19; 1e6 gc 4/8/16 = 8.5/8.4/11.9; 1e7 gc 4/8/12/16 =
-      // 731/712/980/1070: cells larger than the sources' reach gain no
-      // skips, while a cell tile's time span, 256 gc^2 / n of the catalog,
-      // sets how many tiles straddle a block's rows); every cell wastes at
-      // most one partial tile
-      int gc = n < 150000 ? 1 : n < 600000 ? 2 : n < 900000 ? 4 : 8;
+      // by catalog size (measured with 2 rows/thread and 32768-row windows,
+      // trigger ms bench / county catalog: N=5e4 gc 1/2/4 = 0.165/0.161/0.172,
+      // 0.281/0.314/0.323; 1e5 gc 1/2/4 = 0.34/0.29/0.28, 0.78/0.85/0.83;
+      // 3e5 gc 2/4/8 = 1.12/0.95/0.94, 5.31/5.08/4.98; 1e6 gc 4/8/16 (two
+      // classes) = 6.0/5.7/6.7, 44.9/45.1/47.2; 1e7 gc 8/16 = 514/574: cells
+      // larger than the sources' reach gain no skips, while a cell tile's
+      // time span, 256 gc^2 / n of the catalog, sets how many tiles straddle
+      // a block's rows); every cell wastes at most one partial tile
+      int gc = n < 75000 ? 1 : n < 200000 ? 4 : 8;
       if (const char* e = std::getenv("HK_CELL_GC")) gc = std::min(64, std::max(1, std::atoi(e)));  // tuning
       // reach classes: each cell's sources split into bands of log density
       // (a source's reach scales as 1/sqrt(q)), so a cell tile's largest
       // threshold is not set by one low-density source among many local ones
-      // (N=1e6, trigger ms for 1/2/4/8 classes: bench catalog
-      // 8.37/8.21/8.27/8.46, county 52.8/51.5/51.6/52.6; N=1e5 county with 4:
-      // 1.06 -> 1.17): two from gc = 8
+      // (N=1e6, trigger ms for 1/2/4/8 classes with 4 rows/thread: bench
+      // catalog 8.37/8.21/8.27/8.46, county 52.8/51.5/51.6/52.6; with 2
+      // rows/thread 1/2 classes 6.03/5.66, 47.0/45.1): two from gc = 8
       int ncls = gc >= 8 ? 2 : 1;
       if (const char* e = std::getenv("HK_CELL_CLASSES")) ncls = std::min(16, std::max(1, std::atoi(e)));  // tuning
       double qmin = d[0], qmax = d[0];
