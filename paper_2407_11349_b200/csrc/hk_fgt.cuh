@@ -23,6 +23,8 @@ constexpr int kFgtEvalMinBlocks = HK_FGT_MINB;   // __launch_bounds__ minimum re
 constexpr int kFgtRowsPerThread = HK_FGT_RPT;  // rows per thread (kFgtEvalThreads x this divides kFgtRowBlock)
 constexpr int kFgtCkRows = kFgtBlocks * kFgtRowBlock;  // rows per checkpoint (a power of two)
 constexpr int kFgtLeaf = 32 * kFgtRowsPerThread;       // one warp's rows: a k-d leaf
+static_assert(kFgtCkRows % (kFgtRowsPerThread * kFgtEvalThreads) == 0,
+              "an evaluation CTA's rows lie inside one checkpoint");
 constexpr double kFgtCut = 36.0;       // boxes farther than 6 scaled units are skipped (<= e^-36 per unit weight)
 constexpr double kFgtRowTol = 1e-13;   // certified per-row relative error bound, else recompute directly
 constexpr int kFgtMaxBoxes = 1024;     // larger grids (small sigma_x / wide catalogs): direct path
