@@ -115,23 +115,25 @@ int guarded(Fn&& fn) {
 }
 
 // Row blocks per clustering window of the varying plan: the largest power
-// of two whose window holds at most kMaxClusterWindow rows and leaves at
-// least ~12 windows (N=1e6: 128 blocks of 256 rows; N=1e5: 32).  With the
-// cell layout the trigger wants the largest windows the clustering can hold
-// (more rows per window: spatially smaller k-d leaves of 64 rows): bench /
-// county catalog trigger ms at N=1e6, 2 rows/thread, 64 blocks 7.95 / 51.2,
-// 128 blocks 5.66 / 45.0; N=1e5 16 blocks 0.40, 32 blocks 0.36.
+// of two whose window holds at most kMaxSplitWindow rows (median splits first
+// above kMaxClusterWindow, hk::launch_cluster) and leaves at least ~6
+// windows (N=1e6: 512 blocks of 256 rows; N=1e5: 64).  With the cell layout
+// the trigger wants the largest windows (spatially smallest k-d leaves of 64
+// rows; the window's longer time span costs little once whole cell tiles are
+// classified per CTA).  Trigger ms, bench / county catalog: N=1e6 64 blocks
+// 7.95 / 51.2, 128 5.66 / 45.0, 256 4.40 / 42.9, 512 3.79 / 44.1; N=1e5 32
+// blocks 0.28 / 0.83, 64 0.24 / 0.78; N=1e7 256 blocks 379, 512 313.
 // HK_ROW_WINDOW overrides (1 disables the clustering).
 int row_window(int rows) {
   if (const char* e = std::getenv("HK_ROW_WINDOW")) {
     const int w = std::atoi(e);
-    if (w >= 1 && w <= 1024 && (w & (w - 1)) == 0 && w * hk::rows_per_item(true) <= hk::kMaxClusterWindow)
+    if (w >= 1 && w <= 1024 && (w & (w - 1)) == 0 && w * hk::rows_per_item(true) <= hk::kMaxSplitWindow)
       return w;
   }
   const int blocks = (rows + hk::rows_per_item(true) - 1) / hk::rows_per_item(true);
-  const int w_max = hk::kMaxClusterWindow / hk::rows_per_item(true);
+  const int w_max = hk::kMaxSplitWindow / hk::rows_per_item(true);
   int w = 1;
-  while (w < w_max && 2 * w * 12 <= blocks) w *= 2;
+  while (w < w_max && 2 * w * 6 <= blocks) w *= 2;
   return w;
 }
 
@@ -155,6 +157,7 @@ struct DeviceState {
   // clustered row order of the varying plan (hk::launch_cluster), valid for
   // location version rperm_loc
   int* rperm = nullptr;
+  int* cluster_scratch = nullptr;  // row lists of split windows (windows over kMaxClusterWindow rows)
   int window = 1;
   long rperm_loc = -1;
   // work plans per variant (rows per item differ, hk_device.cuh)
@@ -295,6 +298,7 @@ struct hk_ctx {
       if (s.lb) cudaFree(s.lb);
       if (s.ub) cudaFree(s.ub);
       if (s.rperm) cudaFree(s.rperm);
+      if (s.cluster_scratch) cudaFree(s.cluster_scratch);
       for (void* q : {static_cast<void*>(s.cell_id), static_cast<void*>(s.cell_chunk),
                       static_cast<void*>(s.cell_start), static_cast<void*>(s.cell_perm),
                       static_cast<void*>(s.cell_nct), static_cast<void*>(s.cells.xy),
@@ -485,6 +489,8 @@ struct hk_ctx {
       const int wr = s.window * hk::rows_per_item(true);
       const int nb = (re - rb + hk::rows_per_item(true) - 1) / hk::rows_per_item(true);
       s.rperm = dmalloc<int>(static_cast<std::size_t>(hk::window_count(nb, s.window)) * wr);
+      if (wr > hk::kMaxClusterWindow)  // windows split at medians before clustering (hk::launch_cluster)
+        s.cluster_scratch = dmalloc<int>(2 * static_cast<std::size_t>(hk::window_count(nb, s.window)) * wr);
     }
     for (int v = 0; v < 2; ++v) {
       std::vector<hk::Item> items;
@@ -827,7 +833,8 @@ struct hk_ctx {
       const int bi = hk::rows_per_item(true);
       hk::launch_cluster(s.x, s.y, s.rperm, s.rb, rows, s.window * bi,
                          hk::window_count((rows + bi - 1) / bi, s.window),
-                         32 * hk::rows_per_thread(true), c.cx, c.cy, half_extent, s.stream);
+                         32 * hk::rows_per_thread(true), c.cx, c.cy, half_extent, s.stream, 0,
+                         s.cluster_scratch);
       s.rperm_loc = loc_version;
       prof_total += 1;
     }

@@ -1087,18 +1087,41 @@ __device__ __forceinline__ void cluster_window(int rows, int n_windows, int kBI,
 // One CTA per (window, axis): the window sorted along x (blockIdx.y = 0) or y
 // as 16-bit in-window indices, written into the window's own rperm slots
 // (window ints hold both lists) for cluster_kernel.
+// The rows of (sub)window blockIdx.x: rows_base + w0 + i for i < window_rows,
+// or with a list (the halves of a split window, cluster_split_kernel) the
+// list's entries, valid ones first and -1 for padding.
+__device__ __forceinline__ void cluster_rows(const int* list, int window, int rows, int n_windows, int kBI, int& w0,
+                                             int& window_rows) {
+  if (list) {
+    int cnt = 0;
+    for (int i = threadIdx.x; i < window; i += blockDim.x) cnt += list[static_cast<size_t>(blockIdx.x) * window + i] >= 0;
+    __shared__ int s_cnt;
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    atomicAdd(&s_cnt, cnt);  // integer count: order-free
+    __syncthreads();
+    window_rows = s_cnt;
+    w0 = 0;
+    return;
+  }
+  int w1;
+  cluster_window(rows, n_windows, kBI, w0, w1);
+  window_rows = w1 - w0;
+}
+
 __global__ void __launch_bounds__(kClusterThreads)
     cluster_sort_kernel(const double* __restrict__ x, const double* __restrict__ y, int* rperm, int rows_base,
-                        int rows, int window, int n_windows, double cx, double cy, double inv_extent, int kBI) {
+                        int rows, int window, int n_windows, double cx, double cy, double inv_extent, int kBI,
+                        const int* __restrict__ list) {
   unsigned* kc = reinterpret_cast<unsigned*>(s_exp2_tab);  // dynamic shared memory: [window] keys
-  int w0, w1;
-  cluster_window(rows, n_windows, kBI, w0, w1);
-  const int window_rows = w1 - w0;
+  int w0, window_rows;
+  cluster_rows(list, window, rows, n_windows, kBI, w0, window_rows);
   HK_ASSERT(window <= kMaxClusterWindow && window_rows <= window && blockDim.x == kClusterThreads);
   const double* v = blockIdx.y ? y : x;
   const double c = blockIdx.y ? cy : cx;
   for (int i = threadIdx.x; i < window; i += kClusterThreads) {
-    const unsigned q = i < window_rows ? quantise16(v[rows_base + w0 + i], c, inv_extent) : 0xffffu;
+    const int row = list ? list[static_cast<size_t>(blockIdx.x) * window + i] : rows_base + w0 + i;
+    const unsigned q = i < window_rows ? quantise16(v[row], c, inv_extent) : 0xffffu;
     kc[i] = (q << 16) | static_cast<unsigned>(i);
   }
   __syncthreads();
@@ -1109,7 +1132,8 @@ __global__ void __launch_bounds__(kClusterThreads)
 }
 
 __global__ void __launch_bounds__(kClusterThreads)
-    cluster_kernel(int* rperm, int rows_base, int rows, int window, int n_windows, int leaf, int kBI) {
+    cluster_kernel(int* rperm, int rows_base, int rows, int window, int n_windows, int leaf, int kBI,
+                   const int* __restrict__ list, int axis0) {
   // dynamic shared memory (aliases the exp table of other kernels): the
   // x-sorted, y-sorted and scratch index lists, flags [window/32], pre [window/32]
   unsigned short* lx = reinterpret_cast<unsigned short*>(s_exp2_tab);
@@ -1118,9 +1142,8 @@ __global__ void __launch_bounds__(kClusterThreads)
   unsigned* flags = reinterpret_cast<unsigned*>(lt + window);
   int* pre = reinterpret_cast<int*>(flags + window / 32);
   __shared__ int s_wsum[kClusterThreads / 32];
-  int w0, w1;
-  cluster_window(rows, n_windows, kBI, w0, w1);
-  const int window_rows = w1 - w0;
+  int w0, window_rows;
+  cluster_rows(list, window, rows, n_windows, kBI, w0, window_rows);
   const int tid = threadIdx.x, nw = window / 32;
   HK_ASSERT(window <= kMaxClusterWindow && window % leaf == 0 && leaf >= 32 && window_rows <= window &&
             blockDim.x == kClusterThreads && nw <= kClusterThreads);
@@ -1129,9 +1152,9 @@ __global__ void __launch_bounds__(kClusterThreads)
     for (int i = tid; i < 2 * window; i += kClusterThreads) lx[i] = in[i];  // lx then ly
   }
   __syncthreads();
-  unsigned short* sl = lx;  // sorted along this level's axis
-  unsigned short* ol = ly;  // sorted along the other axis
-  unsigned short* nl = lt;  // scratch
+  unsigned short* sl = axis0 ? ly : lx;  // sorted along this level's axis
+  unsigned short* ol = axis0 ? lx : ly;  // sorted along the other axis
+  unsigned short* nl = lt;               // scratch
   for (int S = window; S > leaf; S >>= 1) {
     const int half = S >> 1;
     // membership: the first half of every segment of the split list
@@ -1190,7 +1213,114 @@ __global__ void __launch_bounds__(kClusterThreads)
   }
   for (int i = tid; i < window; i += kClusterThreads) {
     const int e = sl[i];
-    rperm[blockIdx.x * window + i] = e >= window_rows ? -1 : rows_base + w0 + e;
+    rperm[blockIdx.x * window + i] =
+        e >= window_rows ? -1 : (list ? list[static_cast<size_t>(blockIdx.x) * window + e] : rows_base + w0 + e);
+  }
+}
+
+// Windows of up to 2 kMaxClusterWindow rows: one CTA per window splits its
+// rows at the median x into two halves of window/2 slots, written as row
+// lists (valid rows first, -1 padding last) for the halves' clustering along
+// y first (cluster_sort_kernel / cluster_kernel with a list).  The median is
+// a radix select on the 16-bit keys (padding slots carry the largest key):
+// a 256-bin histogram of the high byte, one of the low byte inside the
+// median's bin, then a deterministic partition (keys below the median's go
+// left, equal keys left in index order until the half is full) by two
+// block-wide scans.  O(window) per window.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += t;
+  }
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < static_cast<int>(blockDim.x / 32) ? s_warp[lane] : 0;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, w, off);
+      if (lane >= off) w += t;
+    }
+    s_warp[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  const int ex = inc - v + (warp ? s_warp[warp - 1] : 0);
+  __syncthreads();  // s_warp reusable
+  return ex;
+}
+
+__device__ __forceinline__ unsigned split_key(const double* __restrict__ v, const int* __restrict__ in, size_t base,
+                                              int rows_base, int w0, int i, int window_rows, double c,
+                                              double inv_extent) {
+  if (in) {
+    const int row = in[base + i];
+    return row >= 0 ? quantise16(v[row], c, inv_extent) : 0xffffu;
+  }
+  return i < window_rows ? quantise16(v[rows_base + w0 + i], c, inv_extent) : 0xffffu;
+}
+
+// One CTA per (sub)window: its rows (a contiguous range, or the list `in`)
+// split at the median of coordinate v into the two halves of `out`.
+__global__ void __launch_bounds__(kClusterThreads)
+    cluster_split_kernel(const double* __restrict__ v, const int* __restrict__ in, int* out, int rows_base, int rows,
+                         int window, int n_windows, double c, double inv_extent, int kBI) {
+  __shared__ int s_hist[256];
+  __shared__ int s_warp[32];
+  __shared__ int s_sel[2];
+  const size_t base = static_cast<size_t>(blockIdx.x) * window;
+  int w0 = 0, window_rows = 0;
+  if (!in) {
+    int w1;
+    cluster_window(rows, n_windows, kBI, w0, w1);
+    window_rows = w1 - w0;
+  }
+  const int half = window / 2, tid = threadIdx.x;
+  HK_ASSERT(window % (2 * blockDim.x) == 0 && window <= (1 << 20));
+  // the half-th smallest key (0-based rank half - 1): high byte, then low byte
+  int below = 0, bin = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int b = tid; b < 256; b += blockDim.x) s_hist[b] = 0;
+    __syncthreads();
+    for (int i = tid; i < window; i += blockDim.x) {
+      const unsigned k = split_key(v, in, base, rows_base, w0, i, window_rows, c, inv_extent);
+      if (pass == 0) atomicAdd(&s_hist[k >> 8], 1);  // integer counts: order-free
+      else if ((k >> 8) == static_cast<unsigned>(bin)) atomicAdd(&s_hist[k & 255u], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int acc = below, b = 0;
+      while (acc + s_hist[b] < half) acc += s_hist[b++];
+      s_sel[0] = b;
+      s_sel[1] = acc;
+    }
+    __syncthreads();
+    bin = pass == 0 ? s_sel[0] : (bin << 8) | s_sel[0];
+    below = s_sel[1];
+    __syncthreads();
+  }
+  const unsigned med = static_cast<unsigned>(bin);
+  const int need = half - below;  // keys equal to the median's that go left, in index order
+  // each thread owns a contiguous run of window / blockDim.x slots
+  const int per = window / blockDim.x, i0 = tid * per;
+  int eq = 0;
+  for (int i = i0; i < i0 + per; ++i)
+    eq += split_key(v, in, base, rows_base, w0, i, window_rows, c, inv_extent) == med;
+  int eqr = block_exclusive_scan(eq, s_warp);
+  int left = 0;
+  for (int i = i0; i < i0 + per; ++i) {
+    const unsigned k = split_key(v, in, base, rows_base, w0, i, window_rows, c, inv_extent);
+    left += k < med || (k == med && eqr++ < need);
+  }
+  int lp = block_exclusive_scan(left, s_warp);
+  eqr = block_exclusive_scan(eq, s_warp);
+  for (int i = i0; i < i0 + per; ++i) {
+    const unsigned k = split_key(v, in, base, rows_base, w0, i, window_rows, c, inv_extent);
+    const bool l = k < med || (k == med && eqr++ < need);
+    const int pos = l ? lp++ : half + (i - lp);
+    out[base + pos] = in ? in[base + i] : (i < window_rows ? rows_base + w0 + i : -1);
   }
 }
 
@@ -1544,21 +1674,36 @@ void launch_prep_cells(const DeviceCatalog& d, const EvalCoef& c, const CellLayo
 
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, double half_extent,
-                    cudaStream_t s, int block_rows) {
+                    cudaStream_t s, int block_rows, int* scratch) {
   if (rows <= 0 || n_windows <= 0) return;
-  if (window > kMaxClusterWindow || window < leaf || window % leaf)
+  const bool split = window > kMaxClusterWindow;
+  if (window > kMaxSplitWindow || window < leaf || window % leaf || (split && !scratch))
     throw std::invalid_argument("launch_cluster: unsupported window of " + std::to_string(window) +
                                 " rows");
   const double inv_extent = half_extent > 0.0 ? 1.0 / half_extent : 0.0;
   const int kbi = block_rows > 0 ? block_rows : rows_per_item(true);
-  // the two sorts of every window in parallel CTAs, then the partitions
-  const int sort_bytes = window * 4;
+  int sub = window, nsub = n_windows, axis0 = 0;
+  const int* list = nullptr;
+  // median splits until the (sub)windows fit the shared-memory clustering:
+  // x first, then y, ...; the lists ping-pong between the two scratch halves
+  int* bufs[2] = {scratch, scratch ? scratch + static_cast<size_t>(n_windows) * window : nullptr};
+  for (int level = 0; sub > kMaxClusterWindow; ++level) {
+    int* out = bufs[level & 1];
+    cluster_split_kernel<<<nsub, kClusterThreads, 0, s>>>(axis0 ? y : x, list, out, rows_base, rows, sub,
+                                                          n_windows, axis0 ? cy : cx, inv_extent, kbi);
+    list = out;
+    sub /= 2;
+    nsub *= 2;
+    axis0 ^= 1;
+  }
+  // the two sorts of every (sub)window in parallel CTAs, then the partitions
+  const int sort_bytes = sub * 4;
   cudaFuncSetAttribute(cluster_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_bytes);
-  cluster_sort_kernel<<<dim3(n_windows, 2), kClusterThreads, sort_bytes, s>>>(x, y, rperm, rows_base, rows, window,
-                                                                               n_windows, cx, cy, inv_extent, kbi);
-  const int bytes = window * 6 + (window / 32) * 8;  // lx, ly, scratch, flags, pre (cluster_kernel)
+  cluster_sort_kernel<<<dim3(nsub, 2), kClusterThreads, sort_bytes, s>>>(x, y, rperm, rows_base, rows, sub,
+                                                                          n_windows, cx, cy, inv_extent, kbi, list);
+  const int bytes = sub * 6 + (sub / 32) * 8;  // lx, ly, scratch, flags, pre (cluster_kernel)
   cudaFuncSetAttribute(cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  cluster_kernel<<<n_windows, kClusterThreads, bytes, s>>>(rperm, rows_base, rows, window, n_windows, leaf, kbi);
+  cluster_kernel<<<nsub, kClusterThreads, bytes, s>>>(rperm, rows_base, rows, sub, n_windows, leaf, kbi, list, axis0);
 }
 
 void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, int n_items,

@@ -126,10 +126,14 @@ void launch_prep_cells(const DeviceCatalog& d, const EvalCoef& c, const CellLayo
 // sums: the clustering only lets the density-scaled trigger skip columns per
 // warp.
 // block_rows: the row blocks windows are made of (0: the varying plan's).
+// Windows of more than kMaxClusterWindow rows (up to kMaxSplitWindow) are
+// first split at medians (x, then y, ...) into halves until they fit, which
+// are clustered separately (scratch: 2 * n_windows * window ints).
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, double half_extent,
-                    cudaStream_t s, int block_rows = 0);
-constexpr int kMaxClusterWindow = 32768;  // rows (6.25 bytes each: 200 KB of dynamic shared memory)
+                    cudaStream_t s, int block_rows = 0, int* scratch = nullptr);
+constexpr int kMaxClusterWindow = 32768;  // rows clustered in shared memory (6.25 bytes each: 200 KB)
+constexpr int kMaxSplitWindow = 4 * kMaxClusterWindow;  // rows per window with median splits first
 // Windows of at most max_blocks row blocks covering nblocks: their number,
 // the first block of window w, and the window of block b.
 __host__ __device__ inline int window_count(int nblocks, int max_blocks) {
