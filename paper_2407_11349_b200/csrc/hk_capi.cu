@@ -122,7 +122,8 @@ int guarded(Fn&& fn) {
 // rows; the window's longer time span costs little once whole cell tiles are
 // classified per CTA).  Trigger ms, bench / county catalog: N=1e6 64 blocks
 // 7.95 / 51.2, 128 5.66 / 45.0, 256 4.40 / 42.9, 512 3.79 / 44.1; N=1e5 32
-// blocks 0.28 / 0.83, 64 0.24 / 0.78; N=1e7 256 blocks 379, 512 313.
+// blocks 0.28 / 0.83, 64 0.24 / 0.78; N=1e7 256 blocks 379, 512 313, 1024
+// 266 (at N=1e6, 1024 blocks: 3.51 / 48.7 — the county catalog turns).
 // HK_ROW_WINDOW overrides (1 disables the clustering).
 int row_window(int rows) {
   if (const char* e = std::getenv("HK_ROW_WINDOW")) {

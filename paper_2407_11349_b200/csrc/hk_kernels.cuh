@@ -133,7 +133,7 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
                     int window, int n_windows, int leaf, double cx, double cy, double half_extent,
                     cudaStream_t s, int block_rows = 0, int* scratch = nullptr);
 constexpr int kMaxClusterWindow = 32768;  // rows clustered in shared memory (6.25 bytes each: 200 KB)
-constexpr int kMaxSplitWindow = 4 * kMaxClusterWindow;  // rows per window with median splits first
+constexpr int kMaxSplitWindow = 8 * kMaxClusterWindow;  // rows per window with median splits first
 // Windows of at most max_blocks row blocks covering nblocks: their number,
 // the first block of window w, and the window of block b.
 __host__ __device__ inline int window_count(int nblocks, int max_blocks) {
