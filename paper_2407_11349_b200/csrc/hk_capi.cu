@@ -520,8 +520,9 @@ struct hk_ctx {
       // threshold is not set by one low-density source among many local ones
       // (N=1e6, trigger ms for 1/2/4/8 classes with 4 rows/thread: bench
       // catalog 8.37/8.21/8.27/8.46, county 52.8/51.5/51.6/52.6; with 2
-      // rows/thread 1/2 classes 6.03/5.66, 47.0/45.1): two from gc = 8
-      int ncls = gc >= 8 ? 2 : 1;
+      // rows/thread 1/2 classes 6.03/5.66, 47.0/45.1; with 512-block windows
+      // 2/3 classes 3.80/3.76, 44.1/43.7): three from gc = 8
+      int ncls = gc >= 8 ? 3 : 1;
       if (const char* e = std::getenv("HK_CELL_CLASSES")) ncls = std::min(16, std::max(1, std::atoi(e)));  // tuning
       double qmin = d[0], qmax = d[0];
       for (double v : d) {
