@@ -53,41 +53,43 @@ __global__ void cells_count_kernel(const double* __restrict__ x, const double* _
     chunk_counts[static_cast<size_t>(blockIdx.x) * ncell + c] = s_cnt[c];
 }
 
-// per cell: exclusive prefix over the chunks (in place), the cell's count,
-// then (one thread) the cells' first cell-tile positions.  One warp per cell
-// (cells strided over the CTA's warps), 32 chunks per step.
-constexpr int kScanThreads = 1024;
-__global__ void __launch_bounds__(kScanThreads) cells_scan_kernel(int n_chunks, int ncell, int* chunk_counts,
-                                                                  int* cell_start, int* n_ctiles) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int c = warp; c < ncell; c += kScanThreads / 32) {
-    int carry = 0;
-    for (int k0 = 0; k0 < n_chunks; k0 += 32) {
-      const int k = k0 + lane;
-      int* slot = chunk_counts + static_cast<size_t>(k) * ncell + c;
-      const int v = k < n_chunks ? *slot : 0;
-      int inc = v;
+// per cell (one warp each, a CTA of kScanWarps warps per kScanWarps cells):
+// exclusive prefix over the chunks (in place) and the cell's count, 32
+// chunks per step; then cells_start_kernel turns the counts into the cells'
+// first cell-tile positions.
+constexpr int kScanWarps = 4;
+__global__ void __launch_bounds__(32 * kScanWarps) cells_scan_kernel(int n_chunks, int ncell, int* chunk_counts,
+                                                                     int* cell_count) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * kScanWarps + (threadIdx.x >> 5);
+  if (c >= ncell) return;
+  int carry = 0;
+  for (int k0 = 0; k0 < n_chunks; k0 += 32) {
+    const int k = k0 + lane;
+    int* slot = chunk_counts + static_cast<size_t>(k) * ncell + c;
+    const int v = k < n_chunks ? *slot : 0;
+    int inc = v;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, inc, off);
-        if (lane >= off) inc += t;
-      }
-      if (k < n_chunks) *slot = carry + inc - v;
-      carry += __shfl_sync(0xffffffffu, inc, 31);
+    for (int off = 1; off < 32; off <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += t;
     }
-    if (lane == 0) cell_start[c] = carry;  // the count, for now
+    if (k < n_chunks) *slot = carry + inc - v;
+    carry += __shfl_sync(0xffffffffu, inc, 31);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int pos = 0;
-    for (int c = 0; c < ncell; ++c) {
-      const int cnt = cell_start[c];
-      cell_start[c] = pos;
-      pos += (cnt + kBJ - 1) / kBJ * kBJ;  // whole cell tiles
-    }
-    cell_start[ncell] = pos;
-    *n_ctiles = pos / kBJ;
+  if (lane == 0) cell_count[c] = carry;
+}
+
+__global__ void cells_start_kernel(int ncell, int* cell_start, int* n_ctiles) {
+  if (threadIdx.x != 0) return;
+  int pos = 0;
+  for (int c = 0; c < ncell; ++c) {
+    const int cnt = cell_start[c];  // the count, in place
+    cell_start[c] = pos;
+    pos += (cnt + kBJ - 1) / kBJ * kBJ;  // whole cell tiles
   }
+  cell_start[ncell] = pos;
+  *n_ctiles = pos / kBJ;
 }
 
 // one warp per chunk: stable ranks within the chunk, in index order
@@ -120,7 +122,9 @@ void launch_cells(const double* x, const double* y, const double* q, int n, cons
   const int n_chunks = (n + kRankChunk - 1) / kRankChunk;
   cudaMemsetAsync(perm, 0xff, static_cast<size_t>(perm_len) * sizeof(int), s);  // -1: padding
   cells_count_kernel<<<n_chunks, 256, ncell * sizeof(int), s>>>(x, y, q, n, g, cell, chunk_counts);
-  cells_scan_kernel<<<1, kScanThreads, 0, s>>>(n_chunks, ncell, chunk_counts, cell_start, n_ctiles);
+  cells_scan_kernel<<<(ncell + kScanWarps - 1) / kScanWarps, 32 * kScanWarps, 0, s>>>(n_chunks, ncell, chunk_counts,
+                                                                                      cell_start);
+  cells_start_kernel<<<1, 32, 0, s>>>(ncell, cell_start, n_ctiles);
   cells_rank_kernel<<<n_chunks, 32, ncell * sizeof(int), s>>>(n, ncell, cell, chunk_counts, cell_start, perm);
 }
 
