@@ -1687,7 +1687,10 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
   // median splits until the (sub)windows fit the shared-memory clustering:
   // x first, then y, ...; the lists ping-pong between the two scratch halves
   int* bufs[2] = {scratch, scratch ? scratch + static_cast<size_t>(n_windows) * window : nullptr};
-  for (int level = 0; sub > kMaxClusterWindow; ++level) {
+  // (with a scratch, down to kClusterSplitTarget: the splits are O(n) and
+  // many small shared-memory sorts run in parallel; the k-d tree is the same)
+  const int target = scratch ? kClusterSplitTarget : kMaxClusterWindow;
+  for (int level = 0; sub > target; ++level) {
     int* out = bufs[level & 1];
     cluster_split_kernel<<<nsub, kClusterThreads, 0, s>>>(axis0 ? y : x, list, out, rows_base, rows, sub,
                                                           n_windows, axis0 ? cy : cx, inv_extent, kbi);

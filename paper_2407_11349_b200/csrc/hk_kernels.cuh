@@ -134,6 +134,10 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
                     cudaStream_t s, int block_rows = 0, int* scratch = nullptr);
 constexpr int kMaxClusterWindow = 32768;  // rows clustered in shared memory (6.25 bytes each: 200 KB)
 constexpr int kMaxSplitWindow = 8 * kMaxClusterWindow;  // rows per window with median splits first
+#ifndef HK_CLUSTER_SPLIT_TARGET
+#define HK_CLUSTER_SPLIT_TARGET 8192
+#endif
+constexpr int kClusterSplitTarget = HK_CLUSTER_SPLIT_TARGET;  // split windows down to this many rows
 // Windows of at most max_blocks row blocks covering nblocks: their number,
 // the first block of window w, and the window of block b.
 __host__ __device__ inline int window_count(int nblocks, int max_blocks) {
