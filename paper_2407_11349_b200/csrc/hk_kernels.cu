@@ -269,8 +269,16 @@ __device__ __forceinline__ void tile_fast(RowState<NR>& R, const double* __restr
       }
     }
     if (kTrDense) {
-      const double xj = sx[j], yj = sy[j], wj = sw[j];
-      const double vj = kGrad ? sv[j] : 0.0;
+      double xj, yj, wj, vj;
+      if constexpr (kC) {  // the trigger-only launches' compact layout: {x, y}, {w, K}, {v, z}
+        const double2 xy = reinterpret_cast<const double2*>(buf + cXY * kBJ)[j];
+        xj = xy.x, yj = xy.y;
+        wj = reinterpret_cast<const double2*>(buf + cWK * kBJ)[j].x;
+        vj = kGrad ? reinterpret_cast<const double2*>(buf + cVZ * kBJ)[j].x : 0.0;
+      } else {
+        xj = sx[j], yj = sy[j], wj = sw[j];
+        vj = kGrad ? sv[j] : 0.0;
+      }
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
         const double dx = R.x[r] - xj, dy = R.y[r] - yj;
@@ -579,9 +587,9 @@ __device__ __forceinline__ void tile_masked_cells(RowState<NR>& R, const double*
 // evaluation's background), 2 = trigger only (the density-scaled trigger
 // launch).  Same source, same arithmetic: bitwise the halves of a full launch.
 template <bool kVarying, bool kGrad, int kMode, bool kF32, int kOnly = 0>
-__global__ void __launch_bounds__(kThreads, kOnly == 1   ? 4
-                                            : kOnly == 2 ? HK_MIN_BLOCKS_TRIG
-                                                         : min_blocks(rows_per_thread(kVarying)))
+__global__ void __launch_bounds__(kThreads, kOnly == 1                ? 4
+                                            : kOnly == 2 && kVarying ? HK_MIN_BLOCKS_TRIG
+                                                                      : min_blocks(rows_per_thread(kVarying)))
     pair_kernel(const PairParams P) {
   constexpr int NR = rows_per_thread(kVarying);
   constexpr bool kBgOnly = kOnly == 1, kTrOnly = kOnly == 2;
@@ -1738,6 +1746,17 @@ void launch_pair(const DeviceCatalog& d, const EvalCoef& c, const Item* items, i
       case 6: launch_pair_t<true, false, kExact, true, 2>(P, n_items, s); break;
       case 7: launch_pair_t<true, false, kFlush, true, 2>(P, n_items, s); break;
       default: launch_pair_t<true, false, kChecked, true, 2>(P, n_items, s); break;
+    }
+    return;
+  }
+  if (halves == kHalfTr && !c.varying && !c.single_prec) {  // homogeneous trigger only (the expansion's band)
+    switch ((with_grad ? 3 : 0) + c.mode) {
+      case 0: launch_pair_t<false, false, kExact, false, 2>(P, n_items, s); break;
+      case 1: launch_pair_t<false, false, kFlush, false, 2>(P, n_items, s); break;
+      case 2: launch_pair_t<false, false, kChecked, false, 2>(P, n_items, s); break;
+      case 3: launch_pair_t<false, true, kExact, false, 2>(P, n_items, s); break;
+      case 4: launch_pair_t<false, true, kFlush, false, 2>(P, n_items, s); break;
+      default: launch_pair_t<false, true, kChecked, false, 2>(P, n_items, s); break;
     }
     return;
   }
