@@ -491,7 +491,8 @@ struct hk_ctx {
       const int nb = (re - rb + hk::rows_per_item(true) - 1) / hk::rows_per_item(true);
       s.rperm = dmalloc<int>(static_cast<std::size_t>(hk::window_count(nb, s.window)) * wr);
       if (wr > hk::kClusterSplitTarget)  // windows split at medians before clustering (hk::launch_cluster)
-        s.cluster_scratch = dmalloc<int>(2 * static_cast<std::size_t>(hk::window_count(nb, s.window)) * wr);
+        s.cluster_scratch = dmalloc<int>(2 * static_cast<std::size_t>(hk::window_count(nb, s.window)) * wr +
+                                         hk::cluster_work_ints(hk::window_count(nb, s.window), wr));
     }
     for (int v = 0; v < 2; ++v) {
       std::vector<hk::Item> items;

@@ -1332,6 +1332,143 @@ __global__ void __launch_bounds__(kClusterThreads)
   }
 }
 
+// The same median split with many CTAs per (sub)window: chunks of
+// kSplitChunk slots.  Histograms are summed with integer atomics (order-free),
+// the selection runs per window, and the partition places each chunk's slots
+// from per-chunk counts scanned in chunk order: the output is the
+// single-CTA split's, slot for slot.
+constexpr int kSplitChunk = 4096;
+constexpr int kSplitThreads = 256;
+struct SplitWork {
+  int* hist;  // [nsub][256]
+  int* sel;   // [nsub][4]: bin so far, keys below, median key, equal keys that go left
+  int* cnt;   // [nsub][chunks][2]: keys below the median, keys equal to it
+};
+
+__device__ __forceinline__ unsigned split_key_at(const double* __restrict__ v, const int* __restrict__ in, int sub,
+                                                 int rows_base, int rows, int window, int n_windows, int kBI, int i,
+                                                 double c, double inv_extent) {
+  const size_t base = static_cast<size_t>(sub) * window;
+  if (in) {
+    const int row = in[base + i];
+    return row >= 0 ? quantise16(v[row], c, inv_extent) : 0xffffu;
+  }
+  const int nblocks = (rows + kBI - 1) / kBI;
+  const int w0 = window_first_block(sub, nblocks, n_windows) * kBI;
+  const int w1 = min(rows, window_first_block(sub + 1, nblocks, n_windows) * kBI);
+  return i < w1 - w0 ? quantise16(v[rows_base + w0 + i], c, inv_extent) : 0xffffu;
+}
+
+// pass 0: high-byte histogram; pass 1: low-byte histogram of the keys in the
+// selected high bin
+__global__ void __launch_bounds__(kSplitThreads)
+    split_hist_kernel(const double* __restrict__ v, const int* __restrict__ in, int rows_base, int rows, int window,
+                      int n_windows, int kBI, double c, double inv_extent, SplitWork W, int pass) {
+  __shared__ int s_h[256];
+  const int sub = blockIdx.y, c0 = blockIdx.x * kSplitChunk;
+  for (int b = threadIdx.x; b < 256; b += blockDim.x) s_h[b] = 0;
+  __syncthreads();
+  const int bin = W.sel[sub * 4];
+  for (int i = c0 + threadIdx.x; i < c0 + kSplitChunk; i += blockDim.x) {
+    const unsigned k = split_key_at(v, in, sub, rows_base, rows, window, n_windows, kBI, i, c, inv_extent);
+    if (pass == 0) atomicAdd(&s_h[k >> 8], 1);
+    else if ((k >> 8) == static_cast<unsigned>(bin)) atomicAdd(&s_h[k & 255u], 1);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 256; b += blockDim.x)
+    if (s_h[b]) atomicAdd(&W.hist[sub * 256 + b], s_h[b]);  // integer: order-free
+}
+
+__global__ void split_select_kernel(int window, SplitWork W, int pass) {
+  const int sub = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const int half = window / 2;
+  int acc = pass ? W.sel[sub * 4 + 1] : 0, b = 0;
+  int* h = W.hist + sub * 256;
+  while (acc + h[b] < half) acc += h[b++];
+  for (int k = 0; k < 256; ++k) h[k] = 0;  // ready for the next pass / level
+  if (pass == 0) {
+    W.sel[sub * 4] = b;
+    W.sel[sub * 4 + 1] = acc;
+  } else {
+    const int med = (W.sel[sub * 4] << 8) | b;
+    W.sel[sub * 4 + 2] = med;
+    W.sel[sub * 4 + 3] = half - acc;  // need
+  }
+}
+
+__global__ void __launch_bounds__(kSplitThreads)
+    split_count_kernel(const double* __restrict__ v, const int* __restrict__ in, int rows_base, int rows, int window,
+                       int n_windows, int kBI, double c, double inv_extent, SplitWork W) {
+  __shared__ int s_warp[32];
+  const int sub = blockIdx.y, chunk = blockIdx.x, c0 = chunk * kSplitChunk;
+  const unsigned med = static_cast<unsigned>(W.sel[sub * 4 + 2]);
+  int lt = 0, eq = 0;
+  for (int i = c0 + threadIdx.x; i < c0 + kSplitChunk; i += blockDim.x) {
+    const unsigned k = split_key_at(v, in, sub, rows_base, rows, window, n_windows, kBI, i, c, inv_extent);
+    lt += k < med;
+    eq += k == med;
+  }
+  // block sums (fixed order: integer anyway)
+  const int tl = block_exclusive_scan(lt, s_warp) + lt, te = block_exclusive_scan(eq, s_warp) + eq;
+  if (threadIdx.x == blockDim.x - 1) {
+    const size_t o = (static_cast<size_t>(sub) * gridDim.x + chunk) * 2;
+    W.cnt[o] = tl;
+    W.cnt[o + 1] = te;
+  }
+}
+
+// per window, in chunk order: each chunk's first left position and equal rank
+__global__ void split_scan_kernel(int chunks, SplitWork W) {
+  const int sub = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  const int need = W.sel[sub * 4 + 3];
+  int left = 0, eqb = 0;
+  for (int c = 0; c < chunks; ++c) {
+    int* e = W.cnt + (static_cast<size_t>(sub) * chunks + c) * 2;
+    const int lt = e[0], eq = e[1];
+    const int take = min(max(need - eqb, 0), eq);
+    e[0] = left;  // first left position of the chunk
+    e[1] = eqb;   // equal keys before the chunk
+    left += lt + take;
+    eqb += eq;
+  }
+}
+
+__global__ void __launch_bounds__(kSplitThreads)
+    split_scatter_kernel(const double* __restrict__ v, const int* __restrict__ in, int* out, int rows_base, int rows,
+                         int window, int n_windows, int kBI, double c, double inv_extent, SplitWork W) {
+  __shared__ int s_warp[32];
+  const int sub = blockIdx.y, chunk = blockIdx.x, c0 = chunk * kSplitChunk;
+  const int half = window / 2, per = kSplitChunk / kSplitThreads;
+  const unsigned med = static_cast<unsigned>(W.sel[sub * 4 + 2]);
+  const int need = W.sel[sub * 4 + 3];
+  const int* e = W.cnt + (static_cast<size_t>(sub) * gridDim.x + chunk) * 2;
+  const int i0 = c0 + threadIdx.x * per;  // a contiguous run per thread
+  int eq = 0;
+  for (int i = i0; i < i0 + per; ++i)
+    eq += split_key_at(v, in, sub, rows_base, rows, window, n_windows, kBI, i, c, inv_extent) == med;
+  int eqr = e[1] + block_exclusive_scan(eq, s_warp);
+  const int eqr0 = eqr;
+  int left = 0;
+  for (int i = i0; i < i0 + per; ++i) {
+    const unsigned k = split_key_at(v, in, sub, rows_base, rows, window, n_windows, kBI, i, c, inv_extent);
+    left += k < med || (k == med && eqr++ < need);
+  }
+  int lp = e[0] + block_exclusive_scan(left, s_warp);
+  eqr = eqr0;
+  const size_t base = static_cast<size_t>(sub) * window;
+  const int nblocks = (rows + kBI - 1) / kBI;
+  const int w0 = in ? 0 : window_first_block(sub, nblocks, n_windows) * kBI;
+  const int wr = in ? 0 : min(rows, window_first_block(sub + 1, nblocks, n_windows) * kBI) - w0;
+  for (int i = i0; i < i0 + per; ++i) {
+    const unsigned k = split_key_at(v, in, sub, rows_base, rows, window, n_windows, kBI, i, c, inv_extent);
+    const bool l = k < med || (k == med && eqr++ < need);
+    const int pos = l ? lp++ : half + (i - lp);
+    out[base + pos] = in ? in[base + i] : (i < wr ? rows_base + w0 + i : -1);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // finish + reduce
 
@@ -1695,13 +1832,37 @@ void launch_cluster(const double* x, const double* y, int* rperm, int rows_base,
   // median splits until the (sub)windows fit the shared-memory clustering:
   // x first, then y, ...; the lists ping-pong between the two scratch halves
   int* bufs[2] = {scratch, scratch ? scratch + static_cast<size_t>(n_windows) * window : nullptr};
+  // the multi-CTA splits' histograms, selections and chunk counts (zeroed
+  // here; each selection re-zeroes its histogram for the next pass)
+  int* work = scratch ? scratch + 2 * static_cast<size_t>(n_windows) * window : nullptr;
+  if (work) cudaMemsetAsync(work, 0, cluster_work_ints(n_windows, window) * sizeof(int), s);
   // (with a scratch, down to kClusterSplitTarget: the splits are O(n) and
   // many small shared-memory sorts run in parallel; the k-d tree is the same)
   const int target = scratch ? kClusterSplitTarget : kMaxClusterWindow;
   for (int level = 0; sub > target; ++level) {
     int* out = bufs[level & 1];
-    cluster_split_kernel<<<nsub, kClusterThreads, 0, s>>>(axis0 ? y : x, list, out, rows_base, rows, sub,
-                                                          n_windows, axis0 ? cy : cx, inv_extent, kbi);
+    const double* v = axis0 ? y : x;
+    const double c = axis0 ? cy : cx;
+    if (work && sub % kSplitChunk == 0) {  // many CTAs per window
+      const int chunks = sub / kSplitChunk;
+      // fixed regions sized for the most sub-windows any level has
+      const size_t max_sub = static_cast<size_t>(n_windows) * window / kSplitChunk;
+      SplitWork W{work, work + max_sub * 256, work + max_sub * 260};
+      const dim3 grid(chunks, nsub);
+      for (int pass = 0; pass < 2; ++pass) {
+        split_hist_kernel<<<grid, kSplitThreads, 0, s>>>(v, list, rows_base, rows, sub, n_windows, kbi, c,
+                                                          inv_extent, W, pass);
+        split_select_kernel<<<nsub, 32, 0, s>>>(sub, W, pass);
+      }
+      split_count_kernel<<<grid, kSplitThreads, 0, s>>>(v, list, rows_base, rows, sub, n_windows, kbi, c,
+                                                         inv_extent, W);
+      split_scan_kernel<<<nsub, 32, 0, s>>>(chunks, W);
+      split_scatter_kernel<<<grid, kSplitThreads, 0, s>>>(v, list, out, rows_base, rows, sub, n_windows, kbi, c,
+                                                           inv_extent, W);
+    } else {
+      cluster_split_kernel<<<nsub, kClusterThreads, 0, s>>>(v, list, out, rows_base, rows, sub, n_windows, c,
+                                                            inv_extent, kbi);
+    }
     list = out;
     sub /= 2;
     nsub *= 2;

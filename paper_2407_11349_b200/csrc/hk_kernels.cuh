@@ -126,9 +126,14 @@ void launch_prep_cells(const DeviceCatalog& d, const EvalCoef& c, const CellLayo
 // sums: the clustering only lets the density-scaled trigger skip columns per
 // warp.
 // block_rows: the row blocks windows are made of (0: the varying plan's).
-// Windows of more than kMaxClusterWindow rows (up to kMaxSplitWindow) are
-// first split at medians (x, then y, ...) into halves until they fit, which
-// are clustered separately (scratch: 2 * n_windows * window ints).
+// Windows of more than kClusterSplitTarget rows (up to kMaxSplitWindow) are
+// first split at medians (x, then y, ...) into halves, which are clustered
+// separately (scratch: 2 * n_windows * window + cluster_work_ints ints).
+inline std::size_t cluster_work_ints(int n_windows, int window) {
+  const std::size_t slots = static_cast<std::size_t>(n_windows) * window;
+  // hist [256] + sel [4] for up to slots/4096 sub-windows, then 2 counts per 4096-slot chunk
+  return slots / 4096 * 260 + slots / 2048 + 4096;
+}
 void launch_cluster(const double* x, const double* y, int* rperm, int rows_base, int rows,
                     int window, int n_windows, int leaf, double cx, double cy, double half_extent,
                     cudaStream_t s, int block_rows = 0, int* scratch = nullptr);
